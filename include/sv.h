@@ -1,0 +1,180 @@
+/*
+ * sv.h -- C-ABI of the B200 state-vector gate-application engine (libsv.so).
+ *
+ * The path: load a circuit (IR text) -> classify, fuse and plan passes ->
+ * initialise a 2^n complex state in HBM -> apply the passes with sm_100a kernels ->
+ * read out amplitudes, marginal probabilities or the norm.  Optionally the state is
+ * sharded across P GPUs by its top log2(P) qubits, and dense gates on those "global"
+ * qubits trigger NCCL all-to-all qubit swaps.
+ *
+ * Passages that define the operations (P:n = PAPER.md line n, S:n = SPEC.md line n):
+ *   - P:38 (Background): the state of an n-qubit circuit is a 2^n complex vector of
+ *     amplitudes; each moment is a 2^n x 2^n matrix; a Schroedinger simulator stores all
+ *     amplitudes and its time grows linearly with the number of gates.
+ *   - P:55 (Methods, assumption a): "a quantum circuit simulator is a matrix vector
+ *     multiplication software"; memory and communication dominate at large n.
+ *   - P:123: multi-GPU simulation is the stated future work (implemented here).
+ *   - S:72-120 (qcore), S:167-206 (kernels), S:542-557 (bindings): operation semantics.
+ *
+ * Conventions (all entry points):
+ *   - extern "C"; every function except sv_memory_estimate / sv_last_error returns an
+ *     sv_status (SV_OK = 0).  No C++ exception crosses the boundary.
+ *   - Little-endian: qubit q is bit q of the basis index.  Inside a
+ *     k-qubit matrix, row/column bit j <-> targets[j] (reading R2).  A gate applies U
+ *     when every control qubit is 1.
+ *   - Amplitudes are interleaved (re, im): SV_C64 = 2 x float32 (8 B per amplitude),
+ *     SV_C128 = 2 x float64 (16 B per amplitude).
+ *   - Pointers named host* are host memory borrowed for the duration of the call only.
+ *     Device memory of a state is owned by the handle (sv_create) or borrowed from the
+ *     caller (sv_wrap); the handle never frees a borrowed buffer.
+ *   - Calls that launch work are asynchronous on the handle's CUDA stream; calls that
+ *     return data to the host (sv_amplitudes, sv_probabilities, sv_norm) synchronise it.
+ *     Asynchronous CUDA/NCCL faults surface at the next synchronising call as SV_ERR_CUDA
+ *     / SV_ERR_NCCL.  An error detected before any launch leaves the handle unchanged.
+ *   - sv_last_error() returns a thread-local message for the last failing call.
+ *   - A handle is single-writer.  Sharded handles are collective: every rank
+ *     makes the same calls in the same order.
+ */
+#ifndef SV_H_
+#define SV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sv_state_s* sv_state;   /* opaque state handle */
+typedef struct sv_plan_s* sv_plan;     /* opaque compiled circuit (parse + fuse + plan) */
+
+typedef enum { SV_C64 = 1, SV_C128 = 2 } sv_dtype;
+
+typedef enum {
+    SV_OK = 0,
+    SV_ERR_ARG = 1,       /* bad argument: null pointer, k > 5, bad dtype, bad option */
+    SV_ERR_RANGE = 2,     /* qubit >= n, duplicate qubits across targets and controls, index range */
+    SV_ERR_RESOURCE = 3,  /* allocation failed; message carries sv_memory_estimate(n) */
+    SV_ERR_PARSE = 4,     /* IR text error; message carries the 1-based line number */
+    SV_ERR_CUDA = 5,      /* CUDA runtime error (possibly from an earlier async launch) */
+    SV_ERR_NCCL = 6,      /* NCCL error */
+    SV_ERR_STATE = 7      /* handle/plan mismatch (e.g. plan compiled for another width) */
+} sv_status;
+
+/* Kernel selection for ablations (sv_run_opts.force_kernel). */
+typedef enum {
+    SV_KERNEL_AUTO = 0,       /* fused multi-stage tile passes (default) */
+    SV_KERNEL_PER_GATE = 1,   /* one single-stage pass per gate (no fusion)  */
+    SV_KERNEL_DENSE = 2       /* one pass per gate, every gate as a generic dense block */
+} sv_kernel;
+
+typedef struct {
+    int fuse;            /* 1 (default) = fuse gates into multi-stage tile passes */
+    int tile_qubits;     /* m, qubits per tile pass; 0 = auto */
+    int max_fused_k;     /* reserved: largest pre-multiplied dense block (0 = none) */
+    int force_kernel;    /* sv_kernel */
+    int check_unitary;   /* 1 = reject matrices with |U^dagger U - I| > 1e-9 */
+    int use_graph;       /* 1 = record the plan's launches into a CUDA graph on first use */
+} sv_run_opts;
+
+typedef struct {
+    uint64_t gates;              /* IR gates applied (= gate count) */
+    uint64_t passes;             /* kernel passes launched */
+    uint64_t stages;             /* register stages across all passes */
+    uint64_t swaps;              /* global<->local qubit swap steps (sharded only) */
+    uint64_t launches;           /* kernels launched by this call */
+    uint64_t hbm_bytes;          /* algorithmic HBM bytes (read + write) of the passes */
+    uint64_t nvlink_bytes;       /* bytes sent per rank in swap steps */
+    double plan_ms;              /* host time spent parsing + planning (sv_apply_circuit) */
+} sv_run_stats;
+
+/* 2^n * bytes-per-amplitude of dtype; saturates at UINT64_MAX (reading R20).
+ * Returns 0 for a bad dtype or n < 0. */
+uint64_t sv_memory_estimate(int n, sv_dtype dtype);
+
+/* Allocate a 2^n-amplitude state on the current CUDA device, initialised to |0...0>
+ * (S:72-80).  1 <= n <= 40.  stream: a cudaStream_t to launch on, or NULL to create a
+ * private non-blocking stream.  SV_ERR_RESOURCE if the allocation fails. */
+sv_status sv_create(int n, sv_dtype dtype, void* stream, sv_state* out);
+
+/* Wrap a caller-owned device buffer of 2^n amplitudes (e.g. a torch tensor).  The
+ * buffer contents are left as they are; the handle never frees it. */
+sv_status sv_wrap(int n, sv_dtype dtype, void* dev_ptr, void* stream, sv_state* out);
+
+/* NCCL bootstrap for sharded states: rank 0 writes a 128-byte unique id into out_128B;
+ * the caller broadcasts it (torch.distributed) to every rank. */
+sv_status sv_nccl_unique_id(void* out_128B);
+
+/* Collective: create a state of n qubits sharded over `world` GPUs (world a power of two
+ * >= 2, one process per GPU).  Rank r holds the 2^(n-g) amplitudes whose top g = log2(world)
+ * physical qubits equal r.  State = |0...0>. */
+sv_status sv_create_sharded(int n, sv_dtype dtype, const void* uid_128B, int world, int rank,
+                            void* stream, sv_state* out);
+
+/* Single-process emulation of a `world`-way sharded state on one GPU (tests): the shards
+ * are slices of one allocation and the all-to-all is device-to-device copies.  Runs the
+ * same planner, qubit map and swap schedule as sv_create_sharded. */
+sv_status sv_create_virtual_sharded(int n, sv_dtype dtype, int world, void* stream, sv_state* out);
+
+sv_status sv_destroy(sv_state s);
+
+sv_status sv_init_zero(sv_state s);
+sv_status sv_init_basis(sv_state s, uint64_t k);        /* |k>, SV_ERR_RANGE if k >= 2^n */
+sv_status sv_init_uniform(sv_state s);                  /* every amplitude 2^(-n/2) */
+
+/* Copy `count` amplitudes (interleaved, state dtype) from host memory into logical
+ * indices [first, first+count).  Sharded: each rank writes the part it holds. */
+sv_status sv_set_amplitudes(sv_state s, uint64_t first, uint64_t count, const void* host);
+
+/* Apply one gate.  mat: 2^k x 2^k complex matrix, row-major, interleaved
+ * (re, im) doubles, rounded to the state dtype before use and copied before return.
+ * 1 <= k <= 5; targets[k]; controls[ncontrols] (may be NULL when ncontrols == 0).
+ * SV_ERR_RANGE on qubit >= n or duplicates across targets and controls. */
+sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets,
+                        const int* controls, int ncontrols);
+
+/* Compile IR text for an n-qubit state of dtype: parse (SV_ERR_PARSE with line number),
+ * classify, fuse, plan.  opts NULL = defaults.  The plan is independent of the state's
+ * contents and can be applied many times. */
+sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts* opts,
+                          sv_plan* out);
+sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uint64_t* stages);
+sv_status sv_plan_destroy(sv_plan p);
+
+/* Apply a compiled plan to a state (asynchronous).  stats may be NULL. */
+sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats);
+
+/* Parse + plan + apply every gate of every moment in order.  opts and stats
+ * may be NULL; stats->gates equals the IR gate count. */
+sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* opts,
+                           sv_run_stats* stats);
+
+/* Read amplitudes [first, first+count) of the logical state into host_out (interleaved,
+ * state dtype).  Synchronises.  Sharded: each rank receives the part of the range it holds
+ * (after the qubit map is made canonical) at host_out + (index - first). */
+sv_status sv_amplitudes(sv_state s, uint64_t first, uint64_t count, void* host_out);
+
+/* Marginal probabilities of the qubit subset: host_out[k] = sum over basis states whose
+ * bit qubits[j] equals bit j of k of |a|^2, accumulated in fp64 in a fixed order
+ * (deterministic), 2^nq doubles.  0 <= nq <= min(n, 28).  Sharded: global value on every rank. */
+sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_out);
+
+/* sqrt(sum |a_i|^2) accumulated in fp64 with a fixed-order tree. */
+sv_status sv_norm(sv_state s, double* out);
+
+sv_status sv_sync(sv_state s);
+
+/* Introspection for the bindings and the bench. */
+sv_status sv_info(sv_state s, int* n, int* n_local, int* world, int* rank, sv_dtype* dtype);
+sv_status sv_device_ptr(sv_state s, void** dev_ptr, uint64_t* local_amps);
+sv_status sv_stream(sv_state s, void** stream);
+/* Current physical position of every logical qubit (phys[q]); identity unless swaps ran. */
+sv_status sv_qubit_map(sv_state s, int* phys_out);
+
+const char* sv_last_error(void);
+const char* sv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SV_H_ */

@@ -1,0 +1,612 @@
+// capi.cpp -- the C-ABI (include/sv.h): handles, init, gate/circuit application, readout.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "comm.hpp"
+#include "state.hpp"
+
+using namespace svb;
+
+namespace {
+
+thread_local std::string g_err;
+
+sv_status fail(sv_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+}  // namespace
+
+sv_status svb_fail(sv_status st, const std::string& msg) { return fail(st, msg); }
+
+namespace {
+
+sv_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(SV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+    } while (0)
+
+bool valid_dtype(sv_dtype d) { return d == SV_C64 || d == SV_C128; }
+
+std::string bytes_str(int n, sv_dtype dt) {
+    char buf[160];
+    const uint64_t b = sv_memory_estimate(n, dt);
+    if (b == UINT64_MAX)
+        snprintf(buf, sizeof buf, "2^%d bytes", n + (dt == SV_C128 ? 4 : 3));
+    else
+        snprintf(buf, sizeof buf, "%llu bytes", (unsigned long long)b);
+    return buf;
+}
+
+RunOpts to_opts(const sv_run_opts* o) {
+    RunOpts r;
+    if (o) {
+        r.fuse = o->fuse != 0;
+        r.tile_qubits = o->tile_qubits;
+        r.force_kernel = o->force_kernel;
+        r.check_unitary = o->check_unitary != 0;
+        r.use_graph = o->use_graph != 0;
+    }
+    return r;
+}
+
+Context ctx_of(const sv_state_s* s, int rank) {
+    Context c;
+    c.n = s->n;
+    c.nl = s->nl;
+    c.world = s->world;
+    c.rank = rank;
+    c.phys = s->phys;
+    c.dbl = s->dbl;
+    return c;
+}
+
+sv_status ensure_scratch(sv_state_s* s, size_t doubles) {
+    if (s->scratch_doubles >= doubles) return SV_OK;
+    if (s->d_scratch) cudaFree(s->d_scratch);
+    s->d_scratch = nullptr;
+    s->scratch_doubles = 0;
+    CK(cudaMalloc(&s->d_scratch, doubles * sizeof(double)));
+    s->scratch_doubles = doubles;
+    return SV_OK;
+}
+
+sv_status new_state(int n, int nl, int world, int rank, sv_dtype dt, void* stream, sv_state_s** out) {
+    auto* s = new sv_state_s();
+    s->n = n;
+    s->nl = nl;
+    s->world = world;
+    s->rank = rank;
+    s->g = n - nl;
+    s->dtype = dt;
+    s->dbl = dt == SV_C128;
+    s->phys.resize(n);
+    for (int q = 0; q < n; ++q) s->phys[q] = q;
+    cudaGetDevice(&s->device);
+    if (stream) {
+        s->stream = (cudaStream_t)stream;
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete s;
+            return cuda_fail(e, "cudaStreamCreate");
+        }
+        s->own_stream = true;
+    }
+    *out = s;
+    return SV_OK;
+}
+
+void free_state(sv_state_s* s) {
+    if (!s) return;
+    if (s->owned && s->d) cudaFree(s->d);
+    if (s->d_scratch) cudaFree(s->d_scratch);
+    if (s->xbuf) cudaFree(s->xbuf);
+    if (s->comm) comm_destroy(s->comm);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+double uniform_amp(int n) {
+    // 2^(-n/2): exact power of two for even n, scaled fl(1/sqrt 2) for odd n (App. A)
+    return (n % 2 == 0) ? std::ldexp(1.0, -n / 2) : std::ldexp(0.70710678118654752440, -(n - 1) / 2);
+}
+
+int shard_count(const sv_state_s* s) { return s->virt ? s->world : 1; }
+int shard_rank(const sv_state_s* s, int i) { return s->virt ? i : s->rank; }
+
+sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stats* st) {
+    for (const PassPlan& pp : sc.passes) {
+        cudaError_t e;
+        if (pp.kind == PassPlan::TILE)
+            e = launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles, s->stream);
+        else
+            e = launch_dense_k(s->dbl, psi, pp.params.data(), pp.groups, s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "pass launch");
+        if (st) {
+            st->passes += 1;
+            st->launches += 1;
+            st->stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
+            st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+        }
+    }
+    return SV_OK;
+}
+
+// Make the qubit map the identity (sharded states after swaps); see sharded.cpp.
+sv_status canonicalize(sv_state_s* s) { return sharded_canonicalize(s); }
+
+}  // namespace
+
+// ====================================================================== exported
+extern "C" {
+
+uint64_t sv_memory_estimate(int n, sv_dtype dtype) {
+    if (n < 0 || !valid_dtype(dtype)) return 0;
+    const int sh = dtype == SV_C128 ? 4 : 3;
+    if (n + sh >= 64) return UINT64_MAX;
+    return 1ull << (n + sh);
+}
+
+const char* sv_last_error(void) { return g_err.c_str(); }
+const char* sv_version(void) { return "svb 0.1 (sm_100a)"; }
+
+sv_status sv_create(int n, sv_dtype dtype, void* stream, sv_state* out) {
+    if (!out) return fail(SV_ERR_ARG, "sv_create: out is NULL");
+    if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "sv_create: bad dtype");
+    if (n < 1 || n > 40) return fail(SV_ERR_RANGE, "sv_create: n must be in [1, 40]");
+    sv_state_s* s;
+    sv_status st = new_state(n, n, 1, 0, dtype, stream, &s);
+    if (st != SV_OK) return st;
+    const size_t bytes = (size_t)sv_memory_estimate(n, dtype);
+    cudaError_t e = cudaMalloc(&s->d, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_state(s);
+        return fail(SV_ERR_RESOURCE, "sv_create: cannot allocate the state: needs " + bytes_str(n, dtype) +
+                                         " (" + cudaGetErrorString(e) + ")");
+    }
+    s->owned = true;
+    st = sv_init_zero(s);
+    if (st != SV_OK) {
+        free_state(s);
+        return st;
+    }
+    *out = s;
+    return SV_OK;
+}
+
+sv_status sv_wrap(int n, sv_dtype dtype, void* dev_ptr, void* stream, sv_state* out) {
+    if (!out || !dev_ptr) return fail(SV_ERR_ARG, "sv_wrap: NULL argument");
+    if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "sv_wrap: bad dtype");
+    if (n < 1 || n > 40) return fail(SV_ERR_RANGE, "sv_wrap: n must be in [1, 40]");
+    sv_state_s* s;
+    sv_status st = new_state(n, n, 1, 0, dtype, stream, &s);
+    if (st != SV_OK) return st;
+    s->d = dev_ptr;
+    *out = s;
+    return SV_OK;
+}
+
+sv_status sv_create_virtual_sharded(int n, sv_dtype dtype, int world, void* stream, sv_state* out) {
+    if (!out) return fail(SV_ERR_ARG, "NULL out");
+    if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
+    if (world < 2 || (world & (world - 1))) return fail(SV_ERR_ARG, "world must be a power of two >= 2");
+    int g = 0;
+    while ((1 << g) < world) ++g;
+    if (n - g < 1 || n > 40) return fail(SV_ERR_RANGE, "bad n for this world size");
+    sv_state_s* s;
+    sv_status st = new_state(n, n - g, world, 0, dtype, stream, &s);
+    if (st != SV_OK) return st;
+    s->virt = true;
+    const size_t bytes = (size_t)sv_memory_estimate(n, dtype);
+    cudaError_t e = cudaMalloc(&s->d, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&s->xbuf, bytes / world);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_state(s);
+        return fail(SV_ERR_RESOURCE, "cannot allocate the state: needs " + bytes_str(n, dtype));
+    }
+    s->xbuf_bytes = bytes / world;
+    s->owned = true;
+    st = sv_init_zero(s);
+    if (st != SV_OK) {
+        free_state(s);
+        return st;
+    }
+    *out = s;
+    return SV_OK;
+}
+
+sv_status sv_nccl_unique_id(void* out_128B) {
+    if (!out_128B) return fail(SV_ERR_ARG, "NULL out");
+    std::string err;
+    const sv_status st = comm_unique_id(out_128B, err);
+    if (st != SV_OK) return fail(st, err);
+    return SV_OK;
+}
+
+sv_status sv_create_sharded(int n, sv_dtype dtype, const void* uid, int world, int rank, void* stream,
+                            sv_state* out) {
+    if (!out || !uid) return fail(SV_ERR_ARG, "NULL argument");
+    if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
+    if (world < 2 || (world & (world - 1)) || rank < 0 || rank >= world)
+        return fail(SV_ERR_ARG, "world must be a power of two >= 2 and 0 <= rank < world");
+    int g = 0;
+    while ((1 << g) < world) ++g;
+    if (n - g < 1 || n > 44) return fail(SV_ERR_RANGE, "bad n for this world size");
+    sv_state_s* s;
+    sv_status st = new_state(n, n - g, world, rank, dtype, stream, &s);
+    if (st != SV_OK) return st;
+    const size_t bytes = (size_t)s->local_amps() * s->amp_bytes();
+    cudaError_t e = cudaMalloc(&s->d, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_state(s);
+        return fail(SV_ERR_RESOURCE, "cannot allocate the local shard: needs " + std::to_string(bytes) +
+                                         " bytes per GPU (" + bytes_str(n, dtype) + " total)");
+    }
+    s->owned = true;
+    std::string err;
+    st = comm_init(&s->comm, uid, world, rank, err);
+    if (st != SV_OK) {
+        free_state(s);
+        return fail(st, err);
+    }
+    // staging buffer for the chunked exchange: 1/world of the shard (one peer chunk)
+    s->xbuf_bytes = bytes / world;
+    e = cudaMalloc(&s->xbuf, s->xbuf_bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_state(s);
+        return fail(SV_ERR_RESOURCE, "cannot allocate the exchange buffer (" + std::to_string(bytes / world) + " bytes)");
+    }
+    st = sv_init_zero(s);
+    if (st != SV_OK) {
+        free_state(s);
+        return st;
+    }
+    *out = s;
+    return SV_OK;
+}
+
+sv_status sv_destroy(sv_state s) {
+    free_state(s);
+    return SV_OK;
+}
+
+sv_status sv_init_zero(sv_state s) { return sv_init_basis(s, 0); }
+
+sv_status sv_init_basis(sv_state s, uint64_t k) {
+    if (!s) return fail(SV_ERR_ARG, "NULL state");
+    if (s->n < 64 && k >= (1ull << s->n)) return fail(SV_ERR_RANGE, "basis index out of range");
+    for (int q = 0; q < s->n; ++q) s->phys[q] = q;
+    const size_t shard_bytes = (size_t)s->local_amps() * s->amp_bytes();
+    const int owner = (int)(k >> s->nl);
+    const uint64_t local = k & (s->local_amps() - 1);
+    for (int i = 0; i < shard_count(s); ++i) {
+        void* p = s->shard_ptr(i);
+        CK(cudaMemsetAsync(p, 0, shard_bytes, s->stream));
+        if (shard_rank(s, i) == owner) {
+            if (s->dbl) {
+                static const double one[2] = {1.0, 0.0};
+                CK(cudaMemcpyAsync((char*)p + local * 16, one, 16, cudaMemcpyHostToDevice, s->stream));
+            } else {
+                static const float one[2] = {1.0f, 0.0f};
+                CK(cudaMemcpyAsync((char*)p + local * 8, one, 8, cudaMemcpyHostToDevice, s->stream));
+            }
+        }
+    }
+    return SV_OK;
+}
+
+sv_status sv_init_uniform(sv_state s) {
+    if (!s) return fail(SV_ERR_ARG, "NULL state");
+    for (int q = 0; q < s->n; ++q) s->phys[q] = q;
+    const double a = uniform_amp(s->n);
+    for (int i = 0; i < shard_count(s); ++i) {
+        cudaError_t e = launch_fill(s->dbl, s->shard_ptr(i), s->local_amps(), a, 0.0, s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "fill");
+    }
+    return SV_OK;
+}
+
+sv_status sv_set_amplitudes(sv_state s, uint64_t first, uint64_t count, const void* host) {
+    if (!s || (!host && count)) return fail(SV_ERR_ARG, "NULL argument");
+    const uint64_t N = 1ull << s->n;
+    if (first > N || count > N - first) return fail(SV_ERR_RANGE, "amplitude range out of bounds");
+    sv_status st = canonicalize(s);
+    if (st != SV_OK) return st;
+    const uint64_t L = s->local_amps();
+    const size_t ab = s->amp_bytes();
+    for (int i = 0; i < shard_count(s); ++i) {
+        const uint64_t lo = (uint64_t)shard_rank(s, i) * L, hi = lo + L;
+        const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
+        if (a >= b) continue;
+        CK(cudaMemcpyAsync((char*)s->shard_ptr(i) + (a - lo) * ab, (const char*)host + (a - first) * ab,
+                           (b - a) * ab, cudaMemcpyHostToDevice, s->stream));
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    return SV_OK;
+}
+
+sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets, const int* controls,
+                        int ncontrols) {
+    if (!s || !mat || !targets || (ncontrols > 0 && !controls) || ncontrols < 0)
+        return fail(SV_ERR_ARG, "sv_apply_gate: NULL argument");
+    if (k < 1 || k > 5) return fail(SV_ERR_ARG, "sv_apply_gate: k must be in [1, 5]");
+    Gate g;
+    for (int j = 0; j < k; ++j) g.targets.push_back(targets[j]);
+    for (int j = 0; j < ncontrols; ++j) g.controls.push_back(controls[j]);
+    std::vector<int> all = g.controls;
+    all.insert(all.end(), g.targets.begin(), g.targets.end());
+    for (size_t a = 0; a < all.size(); ++a) {
+        if (all[a] < 0 || all[a] >= s->n) return fail(SV_ERR_RANGE, "sv_apply_gate: qubit out of range");
+        for (size_t b = 0; b < a; ++b)
+            if (all[a] == all[b]) return fail(SV_ERR_RANGE, "sv_apply_gate: duplicate qubit");
+    }
+    const size_t d = (size_t)1 << k;
+    g.U.resize(d * d);
+    for (size_t i = 0; i < d * d; ++i) g.U[i] = cd(mat[2 * i], mat[2 * i + 1]);
+    sv_plan_s plan;
+    plan.circ.n = s->n;
+    plan.circ.gates.push_back(std::move(g));
+    plan.dtype = s->dtype;
+    plan.opts.fuse = false;
+    return sv_plan_apply(s, &plan, nullptr);
+}
+
+sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts* opts, sv_plan* out) {
+    if (!out || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
+    if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
+    if (opts && (opts->force_kernel < 0 || opts->force_kernel > 2 || opts->tile_qubits < 0))
+        return fail(SV_ERR_ARG, "bad sv_run_opts");
+    auto* p = new sv_plan_s();
+    std::string err;
+    const sv_status st = parse_ir(ir_text, p->circ, err);
+    if (st != SV_OK) {
+        delete p;
+        return fail(st, err);
+    }
+    p->dtype = dtype;
+    p->opts = to_opts(opts);
+    *out = p;
+    return SV_OK;
+}
+
+sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uint64_t* stages) {
+    if (!p) return fail(SV_ERR_ARG, "NULL plan");
+    if (n) *n = p->circ.n;
+    if (gates) *gates = p->circ.gates.size();
+    if (passes) *passes = p->cached ? p->sched.passes.size() : 0;
+    if (stages) *stages = p->cached ? p->sched.stages : 0;
+    return SV_OK;
+}
+
+sv_status sv_plan_destroy(sv_plan p) {
+    if (p && p->graph) cudaGraphExecDestroy(p->graph);
+    delete p;
+    return SV_OK;
+}
+
+sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
+    if (!s || !p) return fail(SV_ERR_ARG, "NULL argument");
+    if (p->circ.n != s->n) return fail(SV_ERR_STATE, "plan width " + std::to_string(p->circ.n) +
+                                                         " does not match state width " + std::to_string(s->n));
+    if (p->dtype != s->dtype) return fail(SV_ERR_STATE, "plan dtype does not match state dtype");
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (s->world > 1) return sharded_apply(s, p, stats);
+    std::string err;
+    if (!p->cached) {
+        const Context ctx = ctx_of(s, 0);
+        std::vector<LOp> ops;
+        for (size_t i = 0; i < p->circ.gates.size(); ++i) {
+            bool needs_global = false;
+            const sv_status st = lower_gate(p->circ.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
+            if (st != SV_OK) return fail(st, err);
+        }
+        const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err);
+        if (st != SV_OK) return fail(st, err);
+        p->cached = true;
+    }
+    sv_status st = SV_OK;
+    if (p->opts.use_graph) {
+        if (!p->graph || p->graph_ptr != s->d || p->graph_stream != s->stream) {
+            if (p->graph) cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+            cudaStream_t cs;
+            CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            cudaStream_t keep = s->stream;
+            s->stream = cs;
+            st = run_schedule(s, s->d, p->sched, nullptr);
+            s->stream = keep;
+            cudaGraph_t gr;
+            cudaError_t e = cudaStreamEndCapture(cs, &gr);
+            cudaStreamDestroy(cs);
+            if (st != SV_OK) return st;
+            if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+            CK(cudaGraphInstantiate(&p->graph, gr, 0));
+            cudaGraphDestroy(gr);
+            p->graph_ptr = s->d;
+            p->graph_stream = s->stream;
+        }
+        CK(cudaGraphLaunch(p->graph, s->stream));
+        if (stats) {
+            sv_run_stats tmp{};
+            // count without launching
+            for (const PassPlan& pp : p->sched.passes) {
+                tmp.passes++;
+                tmp.stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
+            }
+            stats->passes = tmp.passes;
+            stats->stages = tmp.stages;
+            stats->launches = tmp.passes;
+            stats->hbm_bytes = 2ull * s->local_amps() * s->amp_bytes() * tmp.passes;
+        }
+    } else {
+        st = run_schedule(s, s->d, p->sched, stats);
+    }
+    if (stats) stats->gates = p->circ.gates.size();
+    return st;
+}
+
+sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* opts, sv_run_stats* stats) {
+    if (!s || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
+    const auto t0 = std::chrono::steady_clock::now();
+    sv_plan p = nullptr;
+    sv_status st = sv_plan_compile(ir_text, s->dtype, opts, &p);
+    if (st != SV_OK) return st;
+    if (p->circ.n != s->n) {
+        sv_plan_destroy(p);
+        return fail(SV_ERR_STATE, "circuit width does not match the state");
+    }
+    st = sv_plan_apply(s, p, stats);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (stats) stats->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    sv_plan_destroy(p);
+    return st;
+}
+
+sv_status sv_amplitudes(sv_state s, uint64_t first, uint64_t count, void* host_out) {
+    if (!s || (!host_out && count)) return fail(SV_ERR_ARG, "NULL argument");
+    const uint64_t N = 1ull << s->n;
+    if (first > N || count > N - first) return fail(SV_ERR_RANGE, "amplitude range out of bounds");
+    sv_status st = canonicalize(s);
+    if (st != SV_OK) return st;
+    const uint64_t L = s->local_amps();
+    const size_t ab = s->amp_bytes();
+    for (int i = 0; i < shard_count(s); ++i) {
+        const uint64_t lo = (uint64_t)shard_rank(s, i) * L, hi = lo + L;
+        const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
+        if (a >= b) continue;
+        CK(cudaMemcpyAsync((char*)host_out + (a - first) * ab, (const char*)s->shard_ptr(i) + (a - lo) * ab,
+                           (b - a) * ab, cudaMemcpyDeviceToHost, s->stream));
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    return SV_OK;
+}
+
+sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_out) {
+    if (!s || !host_out || (nq > 0 && !qubits)) return fail(SV_ERR_ARG, "NULL argument");
+    if (nq < 0 || nq > s->n || nq > 28) return fail(SV_ERR_RANGE, "nq must be in [0, min(n, 28)]");
+    for (int j = 0; j < nq; ++j) {
+        if (qubits[j] < 0 || qubits[j] >= s->n) return fail(SV_ERR_RANGE, "qubit out of range");
+        for (int i = 0; i < j; ++i)
+            if (qubits[i] == qubits[j]) return fail(SV_ERR_RANGE, "duplicate qubit");
+    }
+    // subset qubits held locally vs. as rank bits
+    std::vector<int> lq, lj, gq, gj;
+    for (int j = 0; j < nq; ++j) {
+        const int p = s->phys[qubits[j]];
+        if (p < s->nl) { lq.push_back(p); lj.push_back(j); }
+        else { gq.push_back(p); gj.push_back(j); }
+    }
+    const int nql = (int)lq.size();
+    MarginalParams P{};
+    P.nq = nql;
+    for (int j = 0; j < nql; ++j) P.q[j] = lq[j];
+    std::vector<int> so = lq;
+    std::sort(so.begin(), so.end());
+    for (int j = 0; j < nql; ++j) P.sorted[j] = so[j];
+    const uint64_t rest = 1ull << (s->nl - nql);
+    P.per_chunk = std::min<uint64_t>(rest, 1ull << 13);
+    P.chunks = rest / P.per_chunk;
+    const uint64_t nk = 1ull << nql;
+    const int shards = shard_count(s);
+    sv_status st = ensure_scratch(s, nk * P.chunks + nk * shards);
+    if (st != SV_OK) return st;
+    double* partial = s->d_scratch;
+    double* outs = s->d_scratch + nk * P.chunks;
+    for (int i = 0; i < shards; ++i) {
+        cudaError_t e = launch_marginal(s->dbl, s->shard_ptr(i), P, partial, outs + nk * i, s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "marginal");
+    }
+    std::vector<double> loc(nk * shards);
+    CK(cudaMemcpyAsync(loc.data(), outs, nk * shards * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    // per-rank local marginals (fixed rank order), real sharding gathers them first
+    std::vector<double> all;
+    std::vector<int> ranks;
+    if (s->virt || s->world == 1) {
+        all = loc;
+        for (int i = 0; i < shards; ++i) ranks.push_back(shard_rank(s, i));
+    } else {
+        std::string err;
+        st = comm_allgather_doubles(s, loc.data(), nk, all, err);
+        if (st != SV_OK) return fail(st, err);
+        for (int r = 0; r < s->world; ++r) ranks.push_back(r);
+    }
+    const size_t nout = (size_t)1 << nq;
+    for (size_t k = 0; k < nout; ++k) host_out[k] = 0.0;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+        const int r = ranks[i];
+        size_t kg = 0;
+        for (size_t j = 0; j < gq.size(); ++j)
+            if ((r >> (gq[j] - s->nl)) & 1) kg |= (size_t)1 << gj[j];
+        for (uint64_t kl = 0; kl < nk; ++kl) {
+            size_t k = kg;
+            for (int j = 0; j < nql; ++j)
+                if ((kl >> j) & 1) k |= (size_t)1 << lj[j];
+            host_out[k] += all[i * nk + kl];
+        }
+    }
+    return SV_OK;
+}
+
+sv_status sv_norm(sv_state s, double* out) {
+    if (!s || !out) return fail(SV_ERR_ARG, "NULL argument");
+    double p = 0;
+    const sv_status st = sv_probabilities(s, nullptr, 0, &p);
+    if (st != SV_OK) return st;
+    *out = std::sqrt(p);
+    return SV_OK;
+}
+
+sv_status sv_sync(sv_state s) {
+    if (!s) return fail(SV_ERR_ARG, "NULL state");
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaGetLastError());
+    return SV_OK;
+}
+
+sv_status sv_info(sv_state s, int* n, int* n_local, int* world, int* rank, sv_dtype* dtype) {
+    if (!s) return fail(SV_ERR_ARG, "NULL state");
+    if (n) *n = s->n;
+    if (n_local) *n_local = s->nl;
+    if (world) *world = s->world;
+    if (rank) *rank = s->rank;
+    if (dtype) *dtype = s->dtype;
+    return SV_OK;
+}
+
+sv_status sv_device_ptr(sv_state s, void** dev_ptr, uint64_t* local_amps) {
+    if (!s) return fail(SV_ERR_ARG, "NULL state");
+    if (dev_ptr) *dev_ptr = s->d;
+    if (local_amps) *local_amps = s->virt ? (1ull << s->n) : s->local_amps();
+    return SV_OK;
+}
+
+sv_status sv_stream(sv_state s, void** stream) {
+    if (!s || !stream) return fail(SV_ERR_ARG, "NULL argument");
+    *stream = s->stream;
+    return SV_OK;
+}
+
+sv_status sv_qubit_map(sv_state s, int* phys_out) {
+    if (!s || !phys_out) return fail(SV_ERR_ARG, "NULL argument");
+    for (int q = 0; q < s->n; ++q) phys_out[q] = s->phys[q];
+    return SV_OK;
+}
+
+}  // extern "C"

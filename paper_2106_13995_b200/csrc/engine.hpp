@@ -1,0 +1,94 @@
+// engine.hpp -- host side of the engine: IR, lowering, planner, state.
+#pragma once
+#include <complex>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sv.h"
+#include "sv_internal.hpp"
+#include "sv_kernels.hpp"
+
+namespace svb {
+
+using cd = std::complex<double>;
+
+// ------------------------------------------------------------------ IR (SPEC S:139 + R15)
+struct Gate {
+    std::vector<int> targets;    // row/col bit j <-> targets[j]
+    std::vector<int> controls;
+    std::vector<cd> U;           // 2^k x 2^k row-major
+    int line = 0;
+};
+
+struct Circuit {
+    int n = -1;
+    std::vector<Gate> gates;
+};
+
+// Returns SV_OK or SV_ERR_PARSE with "line N: ..." in err.
+sv_status parse_ir(const char* text, Circuit& out, std::string& err);
+// Named gate table; false if unknown.
+bool named_gate(const std::string& name, int& ncontrols, int& k, std::vector<cd>& U);
+
+// ------------------------------------------------------------------ lowered ops
+enum LKind { L_REG = 0, L_DENSEK = 1 };
+
+struct LOp {
+    int kind = OP_NOP;           // OpKind (register op) ...
+    bool densek = false;         // ... or a standalone dense-k pass
+    std::vector<int> tq;         // non-diagonal targets (physical local qubits), matrix bit order
+    std::vector<int> dq;         // diagonal qubits (physical local), table bit order
+    std::vector<int> ctrl;       // control qubits (physical local)
+    std::vector<cd> coef;        // matrix (tq) or diagonal table (dq) or scalar
+    int gate = -1;               // IR gate index
+    uint64_t touched = 0;        // bitmask of all qubits
+};
+
+struct Context {                 // where a plan runs
+    int n = 0;                   // logical qubits
+    int nl = 0;                  // local qubits
+    int world = 1;
+    int rank = 0;
+    std::vector<int> phys;       // logical -> physical
+    bool dbl = false;
+};
+
+struct RunOpts {
+    bool fuse = true;
+    int tile_qubits = 0;
+    int force_kernel = SV_KERNEL_AUTO;
+    bool check_unitary = false;
+    bool use_graph = false;
+};
+
+// Lower one gate to ops on physical local qubits; folds global qubits (rank constants).
+// needs_global: set when a non-diagonal target is global (caller must swap first).
+sv_status lower_gate(const Gate& g, int gi, const Context& ctx, const RunOpts& o, std::vector<LOp>& out,
+                     bool& needs_global, std::string& err);
+
+// ------------------------------------------------------------------ schedule
+struct PassPlan {
+    enum Kind { TILE, DENSE } kind = TILE;
+    int rb = 0, m = 0, nstages = 0;
+    uint64_t ntiles = 0, groups = 0;
+    int nops = 0;
+    uint64_t touched_amps = 0;           // amplitudes read and written (algorithmic bytes / 2 / amp size)
+    std::vector<unsigned char> params;   // PassParams<real> or DenseParams<real> bytes
+};
+
+struct Schedule {
+    std::vector<PassPlan> passes;
+    uint64_t stages = 0;
+};
+
+sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,
+                         std::string& err);
+
+int default_rb(bool dbl, int nl);
+int default_tile_qubits(bool dbl, int nl, int rb);
+
+}  // namespace svb

@@ -1,0 +1,544 @@
+// kernels.cu -- sm_100a kernels of the gate-application path.
+//
+//   tile_pass_kernel<real, RB>   SURVEY K2-K7: one HBM read + one HBM write of the state per
+//                                pass; every gate of the pass is applied in registers
+//                                (bit-insertion grouping; PAPER.md:55 matrix-vector
+//                                product done gate-locally), shared memory only re-distributes
+//                                the tile between register stages.
+//   dense_k_kernel<real>         SURVEY K4: generic controlled 2^k x 2^k block, one group of
+//                                2^k amplitudes per thread (fallback for k = 5 and the
+//                                SV_KERNEL_DENSE ablation).
+//   fill / set kernels           SURVEY K1 (init: zero, basis, uniform 2^(-n/2)).
+//   marginal kernels             SURVEY K8 (fp64 fixed-order probabilities and norm).
+//
+// Roofline: a tile pass moves 2 * 2^n * sizeof(amp) bytes and does
+// sum-over-ops flops; it is HBM-bound while its per-amplitude op cost stays below the
+// FP32 (FP64) ridge.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <type_traits>
+#include <utility>
+
+#include "sv_internal.hpp"
+#include "sv_kernels.hpp"
+
+namespace svb {
+
+template <typename real> struct V2;
+template <> struct V2<float> { using t = float2; };
+template <> struct V2<double> { using t = double2; };
+
+template <typename V> __device__ __forceinline__ V mk(decltype(V::x) x, decltype(V::x) y) { V r; r.x = x; r.y = y; return r; }
+
+// (a) * (c) complex, written out (ac - bd, ad + bc)
+template <typename V, typename R>
+__device__ __forceinline__ V cmul(V a, R cr, R ci) { return mk<V>(a.x * cr - a.y * ci, a.x * ci + a.y * cr); }
+// acc + a * c
+template <typename V, typename R>
+__device__ __forceinline__ V cfma(V acc, V a, R cr, R ci) {
+    acc.x = fma(a.x, cr, acc.x); acc.x = fma(-a.y, ci, acc.x);
+    acc.y = fma(a.x, ci, acc.y); acc.y = fma(a.y, cr, acc.y);
+    return acc;
+}
+
+// ------------------------------------------------------------------ stage op implementations
+template <int RB, int P, typename V, typename F>
+__device__ __forceinline__ void pairs(V* v, uint32_t creg, F&& f) {
+#pragma unroll
+    for (int s = 0; s < (1 << RB); ++s) {
+        if (s & (1 << P)) continue;
+        if ((s & creg) != creg) continue;
+        f(v[s], v[s | (1 << P)]);
+    }
+}
+
+// dispatch a runtime register position to a compile-time one
+template <int RB, typename F>
+__device__ __forceinline__ void dispatch1(int p, F&& f) {
+    switch (p) {
+        case 0: f(std::integral_constant<int, 0>{}); break;
+        case 1: if constexpr (RB > 1) f(std::integral_constant<int, 1>{}); break;
+        case 2: if constexpr (RB > 2) f(std::integral_constant<int, 2>{}); break;
+        case 3: if constexpr (RB > 3) f(std::integral_constant<int, 3>{}); break;
+        case 4: if constexpr (RB > 4) f(std::integral_constant<int, 4>{}); break;
+        default: break;
+    }
+}
+
+template <int RB, typename F>
+__device__ __forceinline__ void dispatch2(int p0, int p1, F&& f) {
+    // requires p0 < p1
+    switch (p0 * 8 + p1) {
+#define D2(a, b) case a * 8 + b: if constexpr (RB > b) f(std::integral_constant<int, a>{}, std::integral_constant<int, b>{}); break;
+        D2(0, 1) D2(0, 2) D2(0, 3) D2(0, 4) D2(1, 2) D2(1, 3) D2(1, 4) D2(2, 3) D2(2, 4) D2(3, 4)
+#undef D2
+        default: break;
+    }
+}
+
+// multiply every register s with bit P set (or all if P < 0) and controls satisfied
+template <int RB, int P, typename V, typename F>
+__device__ __forceinline__ void diag_on(V* v, uint32_t creg, F&& f) {
+#pragma unroll
+    for (int s = 0; s < (1 << RB); ++s) {
+        if (P >= 0 && !(s & (1 << (P < 0 ? 0 : P)))) continue;
+        if ((s & creg) != creg) continue;
+        v[s] = f(v[s]);
+    }
+}
+
+template <typename real, int RB, typename V>
+__device__ __forceinline__ void apply_diag1(V* v, const OpDesc& op, uint64_t gidx, uint32_t creg, int kind,
+                                            real c0r, real c0i, real c1r, real c1i) {
+    const real h = (real)0.70710678118654752440;
+    auto f1 = [&](V a) -> V {
+        switch (kind) {
+            case OP_Z: return mk<V>(-a.x, -a.y);
+            case OP_S: return mk<V>(-a.y, a.x);
+            case OP_SDG: return mk<V>(a.y, -a.x);
+            case OP_T: return mk<V>((a.x - a.y) * h, (a.x + a.y) * h);
+            case OP_TDG: return mk<V>((a.x + a.y) * h, (a.y - a.x) * h);
+            default: return cmul(a, c1r, c1i);  // PHASE, DIAG1 bit=1
+        }
+    };
+    const bool has0 = (kind == OP_DIAG1);
+    if (op.p[0] == kNotReg) {
+        const int b = (int)((gidx >> op.q[0]) & 1);
+        if (b) {
+            diag_on<RB, -1>(v, creg, f1);
+        } else if (has0) {
+            diag_on<RB, -1>(v, creg, [&](V a) { return cmul(a, c0r, c0i); });
+        }
+    } else {
+        dispatch1<RB>(op.p[0], [&](auto PC) {
+            constexpr int P = decltype(PC)::value;
+            diag_on<RB, P>(v, creg, f1);
+            if (has0) {
+#pragma unroll
+                for (int s = 0; s < (1 << RB); ++s) {
+                    if (s & (1 << P)) continue;
+                    if ((s & creg) != creg) continue;
+                    v[s] = cmul(v[s], c0r, c0i);
+                }
+            }
+        });
+    }
+}
+
+template <typename real, int RB>
+__device__ __forceinline__ void run_op(typename V2<real>::t* v, const PassParams<real>& P, int oi, uint64_t gidx) {
+    using V = typename V2<real>::t;
+    const OpDesc op = P.h.op[oi];
+    if ((gidx & op.cmask) != op.cmask) return;
+    const uint32_t creg = op.creg;
+    const real* cf = P.coef + 2 * op.coef;
+    const real h = (real)0.70710678118654752440;
+    const real half = (real)0.5;
+    switch (op.kind) {
+        case OP_U1: {
+            const real m00r = cf[0], m00i = cf[1], m01r = cf[2], m01i = cf[3];
+            const real m10r = cf[4], m10i = cf[5], m11r = cf[6], m11i = cf[7];
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    V o0 = cmul(a, m00r, m00i); o0 = cfma(o0, b, m01r, m01i);
+                    V o1 = cmul(a, m10r, m10i); o1 = cfma(o1, b, m11r, m11i);
+                    a = o0; b = o1;
+                });
+            });
+        } break;
+        case OP_H:
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    V o0 = mk<V>((a.x + b.x) * h, (a.y + b.y) * h);
+                    V o1 = mk<V>((a.x - b.x) * h, (a.y - b.y) * h);
+                    a = o0; b = o1;
+                });
+            });
+            break;
+        case OP_SX:  // 1/2 [[1+i, 1-i], [1-i, 1+i]]: out0 = (p + i q)/2, out1 = (p - i q)/2
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    const real pr = (a.x + b.x) * half, pi = (a.y + b.y) * half;
+                    const real qr = (a.x - b.x) * half, qi = (a.y - b.y) * half;
+                    a = mk<V>(pr - qi, pi + qr);
+                    b = mk<V>(pr + qi, pi - qr);
+                });
+            });
+            break;
+        case OP_SXDG:  // 1/2 [[1-i, 1+i], [1+i, 1-i]]: out0 = (p - i q)/2, out1 = (p + i q)/2
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    const real pr = (a.x + b.x) * half, pi = (a.y + b.y) * half;
+                    const real qr = (a.x - b.x) * half, qi = (a.y - b.y) * half;
+                    a = mk<V>(pr + qi, pi - qr);
+                    b = mk<V>(pr - qi, pi + qr);
+                });
+            });
+            break;
+        case OP_SY:  // 1/2 [[1+i, -1-i], [1+i, 1+i]]: out0 = (1+i) q/2, out1 = (1+i) p/2
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    const real pr = (a.x + b.x) * half, pi = (a.y + b.y) * half;
+                    const real qr = (a.x - b.x) * half, qi = (a.y - b.y) * half;
+                    a = mk<V>(qr - qi, qr + qi);
+                    b = mk<V>(pr - pi, pr + pi);
+                });
+            });
+            break;
+        case OP_SYDG:  // 1/2 [[1-i, 1-i], [-1+i, 1-i]]: out0 = (1-i) p/2, out1 = -(1-i) q/2
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    const real pr = (a.x + b.x) * half, pi = (a.y + b.y) * half;
+                    const real qr = (a.x - b.x) * half, qi = (a.y - b.y) * half;
+                    a = mk<V>(pr + pi, pi - pr);
+                    b = mk<V>(-(qr + qi), qr - qi);
+                });
+            });
+            break;
+        case OP_X:
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) { V t = a; a = b; b = t; });
+            });
+            break;
+        case OP_Y:  // [[0, -i], [i, 0]]
+            dispatch1<RB>(op.p[0], [&](auto PC) {
+                pairs<RB, decltype(PC)::value>(v, creg, [&](V& a, V& b) {
+                    V o0 = mk<V>(b.y, -b.x);
+                    V o1 = mk<V>(-a.y, a.x);
+                    a = o0; b = o1;
+                });
+            });
+            break;
+        case OP_U2:
+            dispatch2<RB>(op.p[0], op.p[1], [&](auto PA, auto PB) {
+                constexpr int A = decltype(PA)::value, B = decltype(PB)::value;
+#pragma unroll
+                for (int s = 0; s < (1 << RB); ++s) {
+                    if (s & ((1 << A) | (1 << B))) continue;
+                    if ((s & creg) != creg) continue;
+                    const int idx[4] = {s, s | (1 << A), s | (1 << B), s | (1 << A) | (1 << B)};
+                    V in[4], out[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) in[c] = v[idx[c]];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        V acc = cmul(in[0], cf[8 * r], cf[8 * r + 1]);
+#pragma unroll
+                        for (int c = 1; c < 4; ++c) acc = cfma(acc, in[c], cf[8 * r + 2 * c], cf[8 * r + 2 * c + 1]);
+                        out[r] = acc;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) v[idx[r]] = out[r];
+                }
+            });
+            break;
+        case OP_SWAP:
+            dispatch2<RB>(op.p[0], op.p[1], [&](auto PA, auto PB) {
+                constexpr int A = decltype(PA)::value, B = decltype(PB)::value;
+#pragma unroll
+                for (int s = 0; s < (1 << RB); ++s) {
+                    if (s & ((1 << A) | (1 << B))) continue;
+                    if ((s & creg) != creg) continue;
+                    V t = v[s | (1 << A)];
+                    v[s | (1 << A)] = v[s | (1 << B)];
+                    v[s | (1 << B)] = t;
+                }
+            });
+            break;
+        case OP_U3:
+            if constexpr (RB >= 3) {
+#pragma unroll
+                for (int s = 0; s < (1 << RB); s += 8) {
+                    if ((s & creg) != creg) continue;
+                    V in[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) in[c] = v[s + c];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        V acc = cmul(in[0], cf[16 * r], cf[16 * r + 1]);
+#pragma unroll
+                        for (int c = 1; c < 8; ++c) acc = cfma(acc, in[c], cf[16 * r + 2 * c], cf[16 * r + 2 * c + 1]);
+                        v[s + r] = acc;
+                    }
+                }
+            }
+            break;
+        case OP_U4:
+            if constexpr (RB >= 4) {
+#pragma unroll
+                for (int s = 0; s < (1 << RB); s += 16) {
+                    if ((s & creg) != creg) continue;
+                    V in[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) in[c] = v[s + c];
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        V acc = cmul(in[0], cf[32 * r], cf[32 * r + 1]);
+#pragma unroll
+                        for (int c = 1; c < 16; ++c) acc = cfma(acc, in[c], cf[32 * r + 2 * c], cf[32 * r + 2 * c + 1]);
+                        // in[] already captured: safe to write
+                        v[s + r] = acc;
+                    }
+                }
+            }
+            break;
+        case OP_PHASE:
+        case OP_DIAG1:
+        case OP_Z: case OP_S: case OP_SDG: case OP_T: case OP_TDG: {
+            const real c0r = cf[0], c0i = cf[1];
+            const real c1r = (op.kind == OP_DIAG1) ? cf[2] : cf[0];
+            const real c1i = (op.kind == OP_DIAG1) ? cf[3] : cf[1];
+            apply_diag1<real, RB>(v, op, gidx, creg, op.kind, c0r, c0i, c1r, c1i);
+        } break;
+        case OP_DIAG2: {
+            const int b0 = (int)((gidx >> op.q[0]) & 1), b1 = (int)((gidx >> op.q[1]) & 1);
+            const int p0 = op.p[0], p1 = op.p[1];
+#pragma unroll
+            for (int s = 0; s < (1 << RB); ++s) {
+                if ((s & creg) != creg) continue;
+                const int i0 = (p0 == kNotReg) ? b0 : ((s >> p0) & 1);
+                const int i1 = (p1 == kNotReg) ? b1 : ((s >> p1) & 1);
+                const int j = i0 | (i1 << 1);
+                v[s] = cmul(v[s], cf[2 * j], cf[2 * j + 1]);
+            }
+        } break;
+        case OP_SCALAR:
+            diag_on<RB, -1>(v, creg, [&](V a) { return cmul(a, cf[0], cf[1]); });
+            break;
+        default:
+            break;
+    }
+}
+
+// XOR swizzle of a tile-local index (linear over GF(2)): spreads the 2^m slots over the
+// shared-memory banks for every register/thread split.
+template <typename real>
+__device__ __forceinline__ uint32_t swz(uint32_t x) { return swizzle_slot(x, sizeof(real) == 4 ? 4 : 3); }
+
+template <typename real, int RB>
+__global__ void __launch_bounds__(256, 1) tile_pass_kernel(typename V2<real>::t* __restrict__ psi,
+                                                           const __grid_constant__ PassParams<real> P) {
+    using V = typename V2<real>::t;
+    constexpr int R = 1 << RB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* sm = reinterpret_cast<V*>(smem_raw);
+
+    const int m = P.h.m;
+    const int tbits = m - RB;
+    const uint32_t t = threadIdx.x;
+    // tile base: insert zero bits at the (ascending) tile qubits into the tile number
+    uint64_t base = (uint64_t)blockIdx.x;
+    for (int b = 0; b < m; ++b) {
+        const int q = P.h.tq[b];
+        const uint64_t low = base & ((1ull << q) - 1);
+        base = ((base >> q) << (q + 1)) | low;
+    }
+    V v[R];
+    const int ns = P.h.nstages;
+    for (int si = 0; si < ns; ++si) {
+        const StageDesc& S = P.h.stage[si];
+        uint32_t tl = 0;
+        uint64_t tg = 0;
+        for (int i = 0; i < tbits; ++i) {
+            if ((t >> i) & 1) {
+                const int b = S.tpos[i];
+                tl |= 1u << b;
+                tg |= 1ull << P.h.tq[b];
+            }
+        }
+        const uint64_t gidx = base | tg;
+        const uint32_t tls = swz<real>(tl);
+        if (si == 0) {
+#pragma unroll
+            for (int s = 0; s < R; ++s) v[s] = psi[gidx + P.h.goff_first[s]];
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int s = 0; s < R; ++s) v[s] = sm[tls ^ S.loff[s]];
+        }
+        for (int oi = S.op_begin; oi < S.op_end; ++oi) run_op<real, RB>(v, P, oi, gidx);
+        if (si == ns - 1) {
+#pragma unroll
+            for (int s = 0; s < R; ++s) psi[gidx + P.h.goff_last[s]] = v[s];
+        } else {
+#pragma unroll
+            for (int s = 0; s < R; ++s) sm[tls ^ S.loff[s]] = v[s];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ generic dense-k (K4)
+template <typename real>
+__global__ void __launch_bounds__(256) dense_k_kernel(typename V2<real>::t* __restrict__ psi,
+                                                      const __grid_constant__ DenseParams<real> P,
+                                                      uint64_t groups) {
+    using V = typename V2<real>::t;
+    const int k = P.k;
+    const int D = 1 << k;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t base = g;
+        for (int j = 0; j < P.nsorted; ++j) {
+            const int q = P.sorted[j];
+            const uint64_t low = base & ((1ull << q) - 1);
+            base = ((base >> q) << (q + 1)) | low;
+        }
+        // controls fixed to 1 (they are in sorted[] and set here)
+        base |= P.cmask;
+        V in[32];
+        for (int c = 0; c < D; ++c) in[c] = psi[base + P.off[c]];
+        for (int r = 0; r < D; ++r) {
+            V acc = cmul(in[0], P.M[2 * (r * D)], P.M[2 * (r * D) + 1]);
+            for (int c = 1; c < D; ++c) acc = cfma(acc, in[c], P.M[2 * (r * D + c)], P.M[2 * (r * D + c) + 1]);
+            psi[base + P.off[r]] = acc;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ init (K1)
+template <typename real>
+__global__ void fill_kernel(typename V2<real>::t* __restrict__ psi, uint64_t N, real re, real im) {
+    using V = typename V2<real>::t;
+    const V val = mk<V>(re, im);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x)
+        psi[i] = val;
+}
+
+// ------------------------------------------------------------------ readout (K8)
+// Block (k, chunk) sums |a|^2 over the rest-indices of one chunk for the subset value k,
+// each thread sequentially over a fixed strided set, then a fixed-order tree in smem.
+template <typename real>
+__global__ void __launch_bounds__(256) marginal_partial_kernel(const typename V2<real>::t* __restrict__ psi,
+                                                               MarginalParams P, double* __restrict__ partial) {
+    __shared__ double red[256];
+    const uint64_t blk = blockIdx.x;
+    const uint64_t k = blk / P.chunks;
+    const uint64_t chunk = blk % P.chunks;
+    // deposit k into the subset positions
+    uint64_t kbits = 0;
+    for (int j = 0; j < P.nq; ++j) kbits |= ((k >> j) & 1ull) << P.q[j];
+    double acc = 0.0;
+    const uint64_t r0 = chunk * P.per_chunk;
+    for (uint64_t r = r0 + threadIdx.x; r < r0 + P.per_chunk; r += blockDim.x) {
+        // insert zero bits at the sorted subset positions into r
+        uint64_t idx = r;
+        for (int j = 0; j < P.nq; ++j) {
+            const int q = P.sorted[j];
+            const uint64_t low = idx & ((1ull << q) - 1);
+            idx = ((idx >> q) << (q + 1)) | low;
+        }
+        const auto a = psi[idx | kbits];
+        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blk] = red[0];
+}
+
+__global__ void __launch_bounds__(256) marginal_final_kernel(const double* __restrict__ partial, uint64_t chunks,
+                                                             double* __restrict__ out) {
+    __shared__ double red[256];
+    const uint64_t k = blockIdx.x;
+    double acc = 0.0;
+    for (uint64_t c = threadIdx.x; c < chunks; c += blockDim.x) acc += partial[k * chunks + c];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = red[0];
+}
+
+// ------------------------------------------------------------------ host launchers
+template <typename real, int RB>
+static cudaError_t launch_tile_rb(void* psi, const void* params, uint64_t ntiles, int threads, size_t smem,
+                                  cudaStream_t st) {
+    auto* fn = tile_pass_kernel<real, RB>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    fn<<<(unsigned)ntiles, threads, smem, st>>>(reinterpret_cast<typename V2<real>::t*>(psi),
+                                                 *reinterpret_cast<const PassParams<real>*>(params));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_pass(bool dbl, int rb, void* psi, const void* params, int m, int nstages, uint64_t ntiles,
+                             cudaStream_t st) {
+    const int threads = 1 << (m - rb);
+    const size_t smem = nstages > 1 ? ((size_t)1 << m) * (dbl ? 16 : 8) : 0;
+    if (threads > 256 || ntiles > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+    if (dbl) {
+        switch (rb) {
+            case 1: return launch_tile_rb<double, 1>(psi, params, ntiles, threads, smem, st);
+            case 2: return launch_tile_rb<double, 2>(psi, params, ntiles, threads, smem, st);
+            case 3: return launch_tile_rb<double, 3>(psi, params, ntiles, threads, smem, st);
+            case 4: return launch_tile_rb<double, 4>(psi, params, ntiles, threads, smem, st);
+            case 5: return launch_tile_rb<double, 5>(psi, params, ntiles, threads, smem, st);
+        }
+    } else {
+        switch (rb) {
+            case 1: return launch_tile_rb<float, 1>(psi, params, ntiles, threads, smem, st);
+            case 2: return launch_tile_rb<float, 2>(psi, params, ntiles, threads, smem, st);
+            case 3: return launch_tile_rb<float, 3>(psi, params, ntiles, threads, smem, st);
+            case 4: return launch_tile_rb<float, 4>(psi, params, ntiles, threads, smem, st);
+            case 5: return launch_tile_rb<float, 5>(psi, params, ntiles, threads, smem, st);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+static unsigned grid_for(uint64_t work, int threads) {
+    uint64_t b = (work + threads - 1) / threads;
+    const uint64_t cap = 148ull * 16;
+    return (unsigned)(b < cap ? (b ? b : 1) : cap);
+}
+
+cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t groups, cudaStream_t st) {
+    const int threads = 256;
+    if (dbl)
+        dense_k_kernel<double><<<grid_for(groups, threads), threads, 0, st>>>(
+            reinterpret_cast<double2*>(psi), *reinterpret_cast<const DenseParams<double>*>(params), groups);
+    else
+        dense_k_kernel<float><<<grid_for(groups, threads), threads, 0, st>>>(
+            reinterpret_cast<float2*>(psi), *reinterpret_cast<const DenseParams<float>*>(params), groups);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(bool dbl, void* psi, uint64_t N, double re, double im, cudaStream_t st) {
+    const int threads = 256;
+    if (dbl)
+        fill_kernel<double><<<grid_for(N, threads), threads, 0, st>>>(reinterpret_cast<double2*>(psi), N, re, im);
+    else
+        fill_kernel<float><<<grid_for(N, threads), threads, 0, st>>>(reinterpret_cast<float2*>(psi), N, (float)re,
+                                                                      (float)im);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, double* partial, double* out,
+                            cudaStream_t st) {
+    const uint64_t nk = 1ull << P.nq;
+    const uint64_t blocks = nk * P.chunks;
+    const int threads = P.per_chunk >= 256 ? 256 : (int)P.per_chunk;
+    if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+    if (dbl)
+        marginal_partial_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(psi), P,
+                                                                          partial);
+    else
+        marginal_partial_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const float2*>(psi), P,
+                                                                         partial);
+    (void)threads;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    marginal_final_kernel<<<(unsigned)nk, 256, 0, st>>>(partial, P.chunks, out);
+    return cudaGetLastError();
+}
+
+}  // namespace svb

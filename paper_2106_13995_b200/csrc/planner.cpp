@@ -1,0 +1,481 @@
+// planner.cpp -- gate classification, global-qubit folding, and pass/stage scheduling
+// (SURVEY 8(a) a2, a4', a5).
+//
+// Classification (per gate, on its matrix, not its name):
+//   diagonal U           -> phase table on (controls, targets); controls and diagonal qubits
+//                           never need to be register/tile qubits: they are predicates or
+//                           factors computed from the amplitude's index (a4').
+//   known 1-qubit U      -> specialised register op (H, SqrtX, SqrtY, their inverses, X, Y)
+//   SWAP                 -> register swap (no floating point)
+//   other k <= 4         -> dense register op; k = 5 -> standalone dense-k pass (K4)
+// Global (sharded) qubits: controls and diagonal targets on them are folded into rank
+// constants; a non-diagonal target on a global qubit is reported back to the caller,
+// which inserts a swap step first.
+//
+// Scheduling (fusion): greedy over the gate list in order.  A pass owns a tile qubit set S
+// (the low qubits for coalescing plus the non-diagonal targets of its gates, |S| <= m); a
+// gate whose qubits meet an earlier deferred gate is deferred too, so every reordering only
+// commutes gates on disjoint qubits (reading R21).  Inside a pass, gates are cut into
+// register stages of RB qubits the same way.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace svb {
+
+namespace {
+
+inline int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+bool is_diag(const std::vector<cd>& U, size_t d) {
+    for (size_t r = 0; r < d; ++r)
+        for (size_t c = 0; c < d; ++c)
+            if (r != c && U[r * d + c] != cd(0, 0)) return false;
+    return true;
+}
+
+bool eq(const std::vector<cd>& U, std::initializer_list<cd> v) {
+    if (U.size() != v.size()) return false;
+    size_t i = 0;
+    for (const cd& x : v)
+        if (U[i++] != x) return false;
+    return true;
+}
+
+uint64_t qmask(const std::vector<int>& qs) {
+    uint64_t m = 0;
+    for (int q : qs) m |= 1ull << q;
+    return m;
+}
+
+}  // namespace
+
+int default_rb(bool dbl, int nl) { return std::max(1, std::min(dbl ? 4 : 5, nl)); }
+
+int default_tile_qubits(bool dbl, int nl, int rb) {
+    // 2^m amplitudes of shared memory per CTA: 64 KiB for both dtypes
+    const int m = dbl ? 12 : 13;
+    return std::min({m, rb + 8, nl});
+}
+
+sv_status lower_gate(const Gate& g, int gi, const Context& ctx, const RunOpts& o, std::vector<LOp>& out,
+                     bool& needs_global, std::string& err) {
+    needs_global = false;
+    const int k = (int)g.targets.size();
+    const size_t d = (size_t)1 << k;
+    if (k < 1 || k > 5 || g.U.size() != d * d) {
+        err = "gate " + std::to_string(gi) + ": bad matrix shape";
+        return SV_ERR_ARG;
+    }
+    if (o.check_unitary) {
+        for (size_t r = 0; r < d; ++r)
+            for (size_t c = 0; c < d; ++c) {
+                cd acc = 0;
+                for (size_t j = 0; j < d; ++j) acc += std::conj(g.U[j * d + r]) * g.U[j * d + c];
+                if (std::abs(acc - cd(r == c ? 1.0 : 0.0, 0)) > 1e-9) {
+                    err = "gate " + std::to_string(gi) + " (line " + std::to_string(g.line) + "): matrix is not unitary";
+                    return SV_ERR_ARG;
+                }
+            }
+    }
+    auto is_global = [&](int p) { return p >= ctx.nl; };
+    auto rank_bit = [&](int p) { return (ctx.rank >> (p - ctx.nl)) & 1; };
+
+    std::vector<int> ctrl;
+    for (int c : g.controls) {
+        const int p = ctx.phys[c];
+        if (is_global(p)) {
+            if (!rank_bit(p)) return SV_OK;  // control is 0 on this whole shard: identity
+        } else {
+            ctrl.push_back(p);
+        }
+    }
+    std::vector<int> pt(k);
+    for (int j = 0; j < k; ++j) pt[j] = ctx.phys[g.targets[j]];
+    bool any_global_target = false;
+    for (int p : pt) any_global_target |= is_global(p);
+
+    const bool dense_mode = (o.force_kernel == SV_KERNEL_DENSE) && !any_global_target;
+    const bool diag = is_diag(g.U, d);
+
+    LOp op;
+    op.gate = gi;
+    op.ctrl = ctrl;
+    if (dense_mode) {
+        op.densek = true;
+        op.tq = pt;
+        op.coef = g.U;
+    } else if (diag) {
+        // restrict the diagonal to the local targets (global target bits are rank constants)
+        std::vector<int> lt, ltj;
+        int gbits = 0;
+        for (int j = 0; j < k; ++j) {
+            if (is_global(pt[j])) gbits |= rank_bit(pt[j]) << j;
+            else { lt.push_back(pt[j]); ltj.push_back(j); }
+        }
+        const int kl = (int)lt.size();
+        std::vector<cd> dl((size_t)1 << kl);
+        for (size_t r = 0; r < dl.size(); ++r) {
+            size_t full = gbits;
+            for (int j = 0; j < kl; ++j)
+                if ((r >> j) & 1) full |= (size_t)1 << ltj[j];
+            dl[r] = g.U[full * d + full];
+        }
+        bool all_one_but_last = true;
+        for (size_t r = 0; r + 1 < dl.size(); ++r) all_one_but_last &= (dl[r] == cd(1, 0));
+        if (kl == 0) {
+            if (dl[0] == cd(1, 0)) return SV_OK;
+            op.kind = OP_SCALAR;
+            op.coef = {dl[0]};
+        } else if (kl >= 2 && all_one_but_last) {
+            // controlled phase on the last local qubit, the others become controls
+            for (int j = 0; j + 1 < kl; ++j) op.ctrl.push_back(lt[j]);
+            lt = {lt.back()};
+            dl = {cd(1, 0), dl.back()};
+        }
+        if (op.kind != OP_SCALAR) {
+            if (lt.size() == 1) {
+                const double r = 0.70710678118654752440;
+                op.dq = lt;
+                if (dl[0] == cd(1, 0)) {
+                    const cd c = dl[1];
+                    if (c == cd(1, 0)) return SV_OK;
+                    if (c == cd(-1, 0)) op.kind = OP_Z;
+                    else if (c == cd(0, 1)) op.kind = OP_S;
+                    else if (c == cd(0, -1)) op.kind = OP_SDG;
+                    else if (c == cd(r, r)) op.kind = OP_T;
+                    else if (c == cd(r, -r)) op.kind = OP_TDG;
+                    else { op.kind = OP_PHASE; op.coef = {c}; }
+                } else {
+                    op.kind = OP_DIAG1;
+                    op.coef = {dl[0], dl[1]};
+                }
+            } else if (lt.size() == 2) {
+                op.kind = OP_DIAG2;
+                op.dq = lt;
+                op.coef = dl;
+            } else {
+                // general diagonal on >= 3 local qubits: a dense block on those qubits
+                const size_t dd = dl.size();
+                std::vector<cd> M(dd * dd, cd(0, 0));
+                for (size_t r = 0; r < dd; ++r) M[r * dd + r] = dl[r];
+                op.tq = lt;
+                op.coef = M;
+                op.kind = lt.size() == 3 ? OP_U3 : lt.size() == 4 ? OP_U4 : OP_NOP;
+                if (op.kind == OP_NOP) op.densek = true;
+            }
+        }
+    } else {
+        if (any_global_target) {
+            needs_global = true;
+            return SV_OK;
+        }
+        op.tq = pt;
+        const cd I(0, 1);
+        if (k == 1) {
+            const std::vector<cd>& U = g.U;
+            std::vector<cd> tmp;
+            int nc_, k_;
+            auto named = [&](const char* nm) {
+                named_gate(nm, nc_, k_, tmp);
+                return U == tmp;
+            };
+            if (named("X")) op.kind = OP_X;
+            else if (named("Y")) op.kind = OP_Y;
+            else if (named("H")) op.kind = OP_H;
+            else if (named("SqrtX")) op.kind = OP_SX;
+            else if (named("SqrtXdg")) op.kind = OP_SXDG;
+            else if (named("SqrtY")) op.kind = OP_SY;
+            else if (named("SqrtYdg")) op.kind = OP_SYDG;
+            else { op.kind = OP_U1; op.coef = U; }
+        } else if (k == 2 && eq(g.U, {1, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 0, 1})) {
+            op.kind = OP_SWAP;
+        } else if (k == 2) {
+            op.kind = OP_U2;
+            op.coef = g.U;
+        } else if (k == 3) {
+            op.kind = OP_U3;
+            op.coef = g.U;
+        } else if (k == 4) {
+            op.kind = OP_U4;
+            op.coef = g.U;
+        } else {
+            op.densek = true;
+            op.coef = g.U;
+        }
+        (void)I;
+    }
+    op.touched = qmask(op.tq) | qmask(op.dq) | qmask(op.ctrl);
+    out.push_back(std::move(op));
+    return SV_OK;
+}
+
+// ------------------------------------------------------------------ pass building
+namespace {
+
+template <typename real>
+void write_dense_params(const LOp& op, const Context& ctx, PassPlan& pp) {
+    pp.kind = PassPlan::DENSE;
+    pp.params.assign(sizeof(DenseParams<real>), 0);
+    auto* P = reinterpret_cast<DenseParams<real>*>(pp.params.data());
+    const int k = (int)op.tq.size();
+    P->k = k;
+    std::vector<int> all = op.ctrl;
+    all.insert(all.end(), op.tq.begin(), op.tq.end());
+    std::sort(all.begin(), all.end());
+    P->nsorted = (int)all.size();
+    for (size_t j = 0; j < all.size(); ++j) P->sorted[j] = all[j];
+    P->cmask = qmask(op.ctrl);
+    const size_t d = (size_t)1 << k;
+    for (size_t r = 0; r < d; ++r) {
+        uint64_t off = 0;
+        for (int j = 0; j < k; ++j)
+            if ((r >> j) & 1) off |= 1ull << op.tq[j];
+        P->off[r] = off;
+    }
+    for (size_t i = 0; i < d * d; ++i) {
+        P->M[2 * i] = (real)op.coef[i].real();
+        P->M[2 * i + 1] = (real)op.coef[i].imag();
+    }
+    pp.groups = 1ull << (ctx.nl - (int)all.size());
+    pp.touched_amps = pp.groups << k;
+    pp.nops = 1;
+}
+
+struct StagePlan {
+    uint64_t R = 0;                 // register qubits (physical mask)
+    std::vector<int> wide;          // U3/U4 targets placed at register positions 0..k-1
+    std::vector<int> ops;           // indices into pass op list
+};
+
+// permute a 4x4 matrix for swapped target order (bit 0 <-> bit 1)
+std::vector<cd> swap_bits_u2(const std::vector<cd>& M) {
+    auto sw = [](int x) { return ((x & 1) << 1) | ((x >> 1) & 1); };
+    std::vector<cd> R(16);
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) R[r * 4 + c] = M[sw(r) * 4 + sw(c)];
+    return R;
+}
+
+template <typename real>
+bool write_tile_params(const std::vector<const LOp*>& ops, const std::vector<StagePlan>& stages, uint64_t S,
+                       int rb, const Context& ctx, PassPlan& pp, std::string& err) {
+    pp.kind = PassPlan::TILE;
+    pp.params.assign(sizeof(PassParams<real>), 0);
+    auto* P = reinterpret_cast<PassParams<real>*>(pp.params.data());
+    PassHeader& h = P->h;
+    std::vector<int> tq;
+    for (int q = 0; q < 64; ++q)
+        if ((S >> q) & 1) tq.push_back(q);
+    const int m = (int)tq.size();
+    if (m > kMaxTileQubits || m < rb) { err = "internal: bad tile size"; return false; }
+    h.m = (uint8_t)m;
+    h.rb = (uint8_t)rb;
+    h.nstages = (uint8_t)stages.size();
+    h.n_local = (uint32_t)ctx.nl;
+    int local_of[64];
+    for (int i = 0; i < 64; ++i) local_of[i] = -1;
+    for (int b = 0; b < m; ++b) { h.tq[b] = (uint8_t)tq[b]; local_of[tq[b]] = b; }
+    const int lb = sizeof(real) == 4 ? 4 : 3;
+    const int R = 1 << rb;
+    int nop = 0, ncoef = 0;
+    for (size_t si = 0; si < stages.size(); ++si) {
+        const StagePlan& sp = stages[si];
+        StageDesc& sd = h.stage[si];
+        // register order: wide-op targets first, then other needed qubits, then padding
+        std::vector<int> rq = sp.wide;
+        for (int q = 0; q < 64; ++q)
+            if (((sp.R >> q) & 1) && std::find(rq.begin(), rq.end(), q) == rq.end()) rq.push_back(q);
+        for (int b = m - 1; b >= 0 && (int)rq.size() < rb; --b)
+            if (std::find(rq.begin(), rq.end(), tq[b]) == rq.end()) rq.push_back(tq[b]);
+        if ((int)rq.size() != rb) { err = "internal: register set size"; return false; }
+        int regpos_of[64];
+        for (int i = 0; i < 64; ++i) regpos_of[i] = -1;
+        for (int j = 0; j < rb; ++j) { sd.rpos[j] = (uint8_t)local_of[rq[j]]; regpos_of[rq[j]] = j; }
+        int ti = 0;
+        for (int b = 0; b < m; ++b)
+            if (regpos_of[tq[b]] < 0) sd.tpos[ti++] = (uint8_t)b;
+        for (int s = 0; s < R; ++s) {
+            uint32_t lo = 0;
+            uint64_t go = 0;
+            for (int j = 0; j < rb; ++j)
+                if ((s >> j) & 1) { lo |= 1u << sd.rpos[j]; go |= 1ull << rq[j]; }
+            sd.loff[s] = (uint16_t)swizzle_slot(lo, lb);
+            if (si == 0) h.goff_first[s] = go;
+            if (si + 1 == stages.size()) h.goff_last[s] = go;
+        }
+        sd.op_begin = (uint16_t)nop;
+        for (int oi : sp.ops) {
+            const LOp& lo = *ops[oi];
+            if (nop >= kMaxOps) { err = "internal: op overflow"; return false; }
+            OpDesc& od = h.op[nop++];
+            od.kind = (uint8_t)lo.kind;
+            for (int j = 0; j < 4; ++j) od.p[j] = kNotReg;
+            std::vector<cd> coef = lo.coef;
+            if (!lo.tq.empty()) {
+                for (size_t j = 0; j < lo.tq.size(); ++j) od.p[j] = (uint8_t)regpos_of[lo.tq[j]];
+                if (lo.kind == OP_U2 && od.p[0] > od.p[1]) {
+                    std::swap(od.p[0], od.p[1]);
+                    coef = swap_bits_u2(coef);
+                }
+                if (lo.kind == OP_SWAP && od.p[0] > od.p[1]) std::swap(od.p[0], od.p[1]);
+                if (lo.kind == OP_U3 || lo.kind == OP_U4)
+                    for (size_t j = 0; j < lo.tq.size(); ++j)
+                        if (od.p[j] != j) { err = "internal: wide op not at positions 0..k-1"; return false; }
+            }
+            for (size_t j = 0; j < lo.dq.size() && j < 2; ++j) {
+                const int rp = regpos_of[lo.dq[j]];
+                od.p[j] = rp >= 0 ? (uint8_t)rp : kNotReg;
+                od.q[j] = (uint8_t)lo.dq[j];
+            }
+            od.creg = 0;
+            od.cmask = 0;
+            for (int c : lo.ctrl) {
+                const int rp = regpos_of[c];
+                if (rp >= 0) od.creg |= (uint8_t)(1u << rp);
+                else od.cmask |= 1ull << c;
+            }
+            od.coef = (uint32_t)ncoef;
+            if ((size_t)ncoef + coef.size() > (size_t)kMaxCoefComplex) { err = "internal: coef overflow"; return false; }
+            for (const cd& c : coef) {
+                P->coef[2 * ncoef] = (real)c.real();
+                P->coef[2 * ncoef + 1] = (real)c.imag();
+                ++ncoef;
+            }
+        }
+        sd.op_end = (uint16_t)nop;
+    }
+    pp.rb = rb;
+    pp.m = m;
+    pp.nstages = (int)stages.size();
+    pp.ntiles = 1ull << (ctx.nl - m);
+    pp.touched_amps = 1ull << ctx.nl;
+    pp.nops = nop;
+    return true;
+}
+
+size_t coef_size(const LOp& op) { return op.coef.size(); }
+
+}  // namespace
+
+sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,
+                         std::string& err) {
+    const bool dbl = ctx.dbl;
+    const int nl = ctx.nl;
+    const int rb = default_rb(dbl, nl);
+    int m_max = o.tile_qubits > 0 ? o.tile_qubits : default_tile_qubits(dbl, nl, rb);
+    m_max = std::max(rb, std::min({m_max, rb + 8, nl, kMaxTileQubits}));
+    const int m_pad = std::min(rb + 8, nl);       // single-stage passes: 256 threads
+    const int L = std::min(dbl ? 4 : 5, nl);      // low qubits: contiguous 256-byte runs
+    const uint64_t lowmask = (L >= 64) ? ~0ull : ((1ull << L) - 1);
+    const bool per_gate = !o.fuse || o.force_kernel != SV_KERNEL_AUTO;
+
+    std::vector<int> remaining(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) {
+        remaining[i] = (int)i;
+        if ((int)ops[i].tq.size() > rb) ops[i].densek = true;  // cannot live in registers
+    }
+
+    auto emit_dense = [&](const LOp& op) {
+        PassPlan pp;
+        if (dbl) write_dense_params<double>(op, ctx, pp);
+        else write_dense_params<float>(op, ctx, pp);
+        out.passes.push_back(std::move(pp));
+    };
+
+    while (!remaining.empty()) {
+        // ---- choose the pass's gates and tile qubits
+        std::vector<int> pass_ops, deferred;
+        uint64_t S = lowmask, blocked = 0;
+        size_t ncoef = 0;
+        const LOp& first = ops[remaining[0]];
+        if (first.densek) {
+            emit_dense(first);
+            remaining.erase(remaining.begin());
+            continue;
+        }
+        for (int idx : remaining) {
+            const LOp& op = ops[idx];
+            const bool full = per_gate ? !pass_ops.empty()
+                                       : (pass_ops.size() >= (size_t)kMaxOps ||
+                                          ncoef + coef_size(op) > (size_t)kMaxCoefComplex);
+            if (op.densek || full || (op.touched & blocked)) {
+                deferred.push_back(idx);
+                blocked |= op.touched;
+                continue;
+            }
+            const uint64_t need = S | qmask(op.tq);
+            if (popc(need) <= m_max && (int)op.tq.size() <= rb) {
+                S = need;
+                pass_ops.push_back(idx);
+                ncoef += coef_size(op);
+            } else {
+                deferred.push_back(idx);
+                blocked |= op.touched;
+            }
+        }
+        // ---- cut the pass into register stages
+        std::vector<StagePlan> stages;
+        std::vector<int> todo(pass_ops.size());
+        for (size_t i = 0; i < pass_ops.size(); ++i) todo[i] = (int)i;
+        std::vector<int> leftover;
+        while (!todo.empty()) {
+            if ((int)stages.size() == kMaxStages) {
+                for (int i : todo) leftover.push_back(pass_ops[i]);
+                break;
+            }
+            StagePlan sp;
+            uint64_t sblocked = 0;
+            std::vector<int> sdef;
+            for (int i : todo) {
+                const LOp& op = ops[pass_ops[i]];
+                if (op.touched & sblocked) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                const bool wide = (op.kind == OP_U3 || op.kind == OP_U4);
+                if (wide && !sp.wide.empty() && sp.wide != op.tq) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                if (wide && sp.wide.empty()) {
+                    // wide targets go to positions 0..k-1; they must not collide with narrow ops' needs
+                    if (popc(sp.R | qmask(op.tq)) > rb) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                }
+                const uint64_t need = sp.R | qmask(op.tq);
+                if (popc(need) <= rb) {
+                    sp.R = need;
+                    sp.ops.push_back(i);
+                    if (wide) sp.wide = op.tq;
+                } else {
+                    sdef.push_back(i);
+                    sblocked |= op.touched;
+                }
+            }
+            stages.push_back(std::move(sp));
+            todo = std::move(sdef);
+        }
+        // ---- tile qubits: pad to m_pad (threads) with the lowest free qubits
+        for (int q = 0; q < nl && popc(S) < std::max(m_pad, rb); ++q) S |= 1ull << q;
+        if (stages.size() > 1) {
+            // multi-stage passes are bounded by shared memory (2^m amplitudes)
+            for (int q = nl - 1; q >= 0 && popc(S) > m_max; --q) {
+                bool used = false;
+                for (const StagePlan& sp : stages) used |= ((sp.R >> q) & 1);
+                if (!used && !((lowmask >> q) & 1)) S &= ~(1ull << q);
+            }
+        }
+        std::vector<const LOp*> pops;  // stage op indices refer to this list
+        for (int idx : pass_ops) pops.push_back(&ops[idx]);
+        PassPlan pp;
+        const bool ok = dbl ? write_tile_params<double>(pops, stages, S, rb, ctx, pp, err)
+                            : write_tile_params<float>(pops, stages, S, rb, ctx, pp, err);
+        if (!ok) return SV_ERR_STATE;
+        out.stages += stages.size();
+        out.passes.push_back(std::move(pp));
+        // ---- next round: leftovers and deferred gates in original order
+        std::vector<int> next = deferred;
+        next.insert(next.end(), leftover.begin(), leftover.end());
+        std::sort(next.begin(), next.end());
+        remaining = std::move(next);
+    }
+    return SV_OK;
+}
+
+}  // namespace svb

@@ -1,0 +1,313 @@
+// sharded.cpp -- the sharded run loop.
+//
+// Rank r holds the 2^nl amplitudes whose top g = log2(P) physical bits equal r.  Gates are
+// lowered against the current logical->physical qubit map; controls and diagonal factors on
+// global qubits fold into rank constants (no communication).  A gate with a non-diagonal
+// target on a global qubit is deferred, together with every later gate that shares a qubit
+// with it (so only disjoint gates are commuted, reading R21); everything else runs.  Then
+// one exchange step swaps the g global bits with the g top local bits: rank r sends its
+// chunk c (top local bits = c) to rank c and receives rank c's chunk r into the same place,
+// pairwise (peer = r XOR k, k = 1..P-1) through a one-chunk staging buffer (N2).  Before
+// the exchange, the local qubits with the farthest next use are moved into the top local
+// positions by physical SWAP ops fused into the last batch (a relabel, no extra pass).
+#include <algorithm>
+#include <cstring>
+
+#include "comm.hpp"
+
+using namespace svb;
+
+namespace {
+
+sv_status set_err(sv_status st, const std::string& m) { return svb_fail(st, m); }
+
+struct ShardRun {
+    std::vector<int> ranks;       // ranks executed in this process
+    std::vector<Schedule> sched;  // one per executed rank
+};
+
+int nshards(const sv_state_s* s) { return s->virt ? s->world : 1; }
+int rank_of(const sv_state_s* s, int i) { return s->virt ? i : s->rank; }
+
+Context make_ctx(const sv_state_s* s, int rank) {
+    Context c;
+    c.n = s->n;
+    c.nl = s->nl;
+    c.world = s->world;
+    c.rank = rank;
+    c.phys = s->phys;
+    c.dbl = s->dbl;
+    return c;
+}
+
+LOp phys_swap(int a, int b) {
+    LOp op;
+    op.kind = OP_SWAP;
+    op.tq = {std::min(a, b), std::max(a, b)};
+    op.touched = (1ull << a) | (1ull << b);
+    return op;
+}
+
+sv_status run_ops(sv_state_s* s, std::vector<std::vector<LOp>>& ops, const RunOpts& o, sv_run_stats* st,
+                  std::string& err) {
+    for (int i = 0; i < nshards(s); ++i) {
+        Schedule sc;
+        const Context ctx = make_ctx(s, rank_of(s, i));
+        sv_status r = build_schedule(ops[i], ctx, o, sc, err);
+        if (r != SV_OK) return r;
+        void* psi = s->shard_ptr(i);
+        for (const PassPlan& pp : sc.passes) {
+            cudaError_t e = pp.kind == PassPlan::TILE
+                                ? launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles,
+                                                   s->stream)
+                                : launch_dense_k(s->dbl, psi, pp.params.data(), pp.groups, s->stream);
+            if (e != cudaSuccess) {
+                err = std::string("pass launch: ") + cudaGetErrorString(e);
+                return SV_ERR_CUDA;
+            }
+            if (st && i == 0) {
+                st->passes++;
+                st->launches++;
+                st->stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
+                st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+            }
+        }
+    }
+    return SV_OK;
+}
+
+// Exchange the g global bits with the g top local bits (whole-block all-to-all, N1/N2).
+sv_status exchange_all(sv_state_s* s, sv_run_stats* st, std::string& err) {
+    const int g = s->g, P = s->world;
+    const size_t chunk = (size_t)(s->local_amps() >> g) * s->amp_bytes();
+    if (s->virt) {
+        for (int r = 0; r < P; ++r)
+            for (int c = r + 1; c < P; ++c) {
+                char* a = (char*)s->shard_ptr(r) + (size_t)c * chunk;
+                char* b = (char*)s->shard_ptr(c) + (size_t)r * chunk;
+                if (cudaMemcpyAsync(s->xbuf, a, chunk, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess ||
+                    cudaMemcpyAsync(a, b, chunk, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess ||
+                    cudaMemcpyAsync(b, s->xbuf, chunk, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
+                    err = "virtual exchange copy failed";
+                    return SV_ERR_CUDA;
+                }
+            }
+    } else {
+        for (int k = 1; k < P; ++k) {
+            const int peer = s->rank ^ k;
+            char* mine = (char*)s->d + (size_t)peer * chunk;
+            sv_status r = comm_sendrecv(s, peer, mine, s->xbuf, chunk, err);
+            if (r != SV_OK) return r;
+            if (cudaMemcpyAsync(mine, s->xbuf, chunk, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
+                err = "exchange unpack copy failed";
+                return SV_ERR_CUDA;
+            }
+        }
+    }
+    // map: logical at physical nl-g+j <-> logical at physical nl+j
+    for (int j = 0; j < g; ++j) {
+        const int a = s->nl - g + j, b = s->nl + j;
+        for (int& p : s->phys) {
+            if (p == a) p = b;
+            else if (p == b) p = a;
+        }
+    }
+    if (st) {
+        st->swaps++;
+        st->nvlink_bytes += (uint64_t)chunk * (P - 1);
+    }
+    return SV_OK;
+}
+
+// Swap one global bit (physical nl+j) with the top local bit (physical nl-1), N3.
+sv_status exchange_one(sv_state_s* s, int j, std::string& err) {
+    const size_t half = (size_t)(s->local_amps() >> 1) * s->amp_bytes();
+    const size_t piece = std::min(half, s->xbuf_bytes);
+    if (s->virt) {
+        for (int r = 0; r < s->world; ++r) {
+            if ((r >> j) & 1) continue;
+            const int p = r | (1 << j);
+            // rank r (bit 0) gives its top half (t=1); rank p (bit 1) gives its low half (t=0)
+            char* a = (char*)s->shard_ptr(r) + half;
+            char* b = (char*)s->shard_ptr(p);
+            for (size_t off = 0; off < half; off += piece) {
+                const size_t len = std::min(piece, half - off);
+                if (cudaMemcpyAsync(s->xbuf, a + off, len, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess ||
+                    cudaMemcpyAsync(a + off, b + off, len, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess ||
+                    cudaMemcpyAsync(b + off, s->xbuf, len, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
+                    err = "virtual exchange copy failed";
+                    return SV_ERR_CUDA;
+                }
+            }
+        }
+    } else {
+        const int b = (s->rank >> j) & 1;
+        const int peer = s->rank ^ (1 << j);
+        char* mine = (char*)s->d + (b ? 0 : half);
+        for (size_t off = 0; off < half; off += piece) {
+            const size_t len = std::min(piece, half - off);
+            sv_status r = comm_sendrecv(s, peer, mine + off, s->xbuf, len, err);
+            if (r != SV_OK) return r;
+            if (cudaMemcpyAsync(mine + off, s->xbuf, len, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
+                err = "exchange unpack copy failed";
+                return SV_ERR_CUDA;
+            }
+        }
+    }
+    const int a = s->nl - 1, c = s->nl + j;
+    for (int& p : s->phys) {
+        if (p == a) p = c;
+        else if (p == c) p = a;
+    }
+    return SV_OK;
+}
+
+uint64_t gate_mask(const Gate& g) {
+    uint64_t m = 0;
+    for (int q : g.targets) m |= 1ull << q;
+    for (int q : g.controls) m |= 1ull << q;
+    return m;
+}
+
+}  // namespace
+
+sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
+    std::string err;
+    const auto& gates = p->circ.gates;
+    std::vector<int> pending(gates.size());
+    for (size_t i = 0; i < gates.size(); ++i) pending[i] = (int)i;
+    RunOpts o = p->opts;
+    if (o.force_kernel == SV_KERNEL_DENSE) o.force_kernel = SV_KERNEL_PER_GATE;  // dense-k needs local targets
+    const int S = nshards(s);
+    while (!pending.empty()) {
+        std::vector<std::vector<LOp>> ops(S);
+        std::vector<int> deferred;
+        uint64_t blocked = 0;
+        for (int gi : pending) {
+            const Gate& g = gates[gi];
+            const uint64_t T = gate_mask(g);
+            if (T & blocked) {
+                deferred.push_back(gi);
+                blocked |= T;
+                continue;
+            }
+            bool needs = false;
+            for (int i = 0; i < S; ++i) {
+                const Context ctx = make_ctx(s, rank_of(s, i));
+                const sv_status r = lower_gate(g, gi, ctx, o, ops[i], needs, err);
+                if (r != SV_OK) return set_err(r, err);
+                if (needs) break;
+            }
+            if (needs) {
+                deferred.push_back(gi);
+                blocked |= T;
+            }
+        }
+        if (!deferred.empty()) {
+            // relabel: put the g local logical qubits with the farthest next use at the top
+            const int g = s->g, nl = s->nl;
+            std::vector<long> next_use(s->n, (long)1 << 40);
+            for (size_t i = deferred.size(); i-- > 0;) {
+                const Gate& gg = gates[deferred[i]];
+                for (int q : gg.targets) next_use[q] = (long)i;
+                for (int q : gg.controls) next_use[q] = (long)i;
+            }
+            std::vector<int> local_logical;
+            for (int q = 0; q < s->n; ++q)
+                if (s->phys[q] < nl) local_logical.push_back(q);
+            std::stable_sort(local_logical.begin(), local_logical.end(), [&](int a, int b) {
+                if (next_use[a] != next_use[b]) return next_use[a] > next_use[b];
+                return s->phys[a] > s->phys[b];  // prefer qubits already high
+            });
+            std::vector<int> F(local_logical.begin(), local_logical.begin() + g);
+            std::vector<int> inF(s->n, 0);
+            for (int q : F) inF[q] = 1;
+            std::vector<int> logical_at(s->n);
+            for (int q = 0; q < s->n; ++q) logical_at[s->phys[q]] = q;
+            for (int q : F) {
+                if (s->phys[q] >= nl - g) continue;
+                // a top-local slot whose occupant is not in F
+                for (int t = nl - g; t < nl; ++t) {
+                    const int occ = logical_at[t];
+                    if (inF[occ]) continue;
+                    const int pq = s->phys[q];
+                    for (int i = 0; i < S; ++i) ops[i].push_back(phys_swap(pq, t));
+                    std::swap(s->phys[q], s->phys[occ]);
+                    logical_at[t] = q;
+                    logical_at[pq] = occ;
+                    break;
+                }
+            }
+        }
+        sv_status r = run_ops(s, ops, o, stats, err);
+        if (r != SV_OK) return set_err(r, err);
+        if (deferred.empty()) break;
+        r = exchange_all(s, stats, err);
+        if (r != SV_OK) return set_err(r, err);
+        if (deferred.size() == pending.size()) {
+            // the exchange must make the first deferred gate runnable; guard against livelock
+            const Gate& g0 = gates[deferred[0]];
+            for (int q : g0.targets)
+                if (s->phys[q] >= s->nl && g0.U.size() > 1) {
+                    bool diag = true;
+                    const size_t d = (size_t)1 << g0.targets.size();
+                    for (size_t a = 0; a < d && diag; ++a)
+                        for (size_t b = 0; b < d; ++b)
+                            if (a != b && g0.U[a * d + b] != cd(0, 0)) { diag = false; break; }
+                    if (!diag) return set_err(SV_ERR_STATE, "sharded planner made no progress");
+                }
+        }
+        pending = std::move(deferred);
+    }
+    if (stats) stats->gates = gates.size();
+    return SV_OK;
+}
+
+// Bring the qubit map back to the identity: single-bit exchanges for the global positions,
+// then a batch of physical SWAP ops for the local positions.
+sv_status sharded_canonicalize(sv_state_s* s) {
+    if (s->world == 1) return SV_OK;
+    std::string err;
+    RunOpts o;
+    const int nl = s->nl, g = s->g;
+    auto relabel = [&](const std::vector<std::pair<int, int>>& sw) -> sv_status {
+        std::vector<std::vector<LOp>> ops(nshards(s));
+        for (auto& pr : sw)
+            for (auto& v : ops) v.push_back(phys_swap(pr.first, pr.second));
+        return run_ops(s, ops, o, nullptr, err);
+    };
+    auto phys_swap_map = [&](int a, int b) {
+        for (int& p : s->phys) {
+            if (p == a) p = b;
+            else if (p == b) p = a;
+        }
+    };
+    for (int j = 0; j < g; ++j) {
+        const int want = s->n - g + j;
+        int p = s->phys[want];
+        if (p == nl + j) continue;
+        sv_status r;
+        if (p >= nl) {
+            r = exchange_one(s, p - nl, err);  // now at nl-1
+            if (r != SV_OK) return set_err(r, err);
+        } else if (p != nl - 1) {
+            r = relabel({{p, nl - 1}});
+            if (r != SV_OK) return set_err(r, err);
+            phys_swap_map(p, nl - 1);
+        }
+        r = exchange_one(s, j, err);
+        if (r != SV_OK) return set_err(r, err);
+    }
+    std::vector<std::pair<int, int>> sw;
+    for (int pos = 0; pos < nl; ++pos) {
+        const int q = s->phys[pos];  // where logical `pos` lives
+        if (q == pos) continue;
+        sw.push_back({pos, q});
+        phys_swap_map(pos, q);
+    }
+    if (!sw.empty()) {
+        const sv_status r = relabel(sw);
+        if (r != SV_OK) return set_err(r, err);
+    }
+    return SV_OK;
+}

@@ -1,0 +1,51 @@
+// state.hpp -- the sv_state / sv_plan objects behind the C-ABI handles.
+#pragma once
+#include <map>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+
+// sets the thread-local sv_last_error() message and returns st (capi.cpp)
+sv_status svb_fail(sv_status st, const std::string& msg);
+
+struct sv_state_s {
+    int n = 0;              // logical qubits
+    int nl = 0;             // local (per-shard) qubits
+    int g = 0;              // global qubits = log2(world)
+    int world = 1;
+    int rank = 0;
+    sv_dtype dtype = SV_C64;
+    bool dbl = false;
+    void* d = nullptr;      // local shard (or the whole virtual allocation)
+    bool owned = false;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool virt = false;      // virtual sharding: all shards in this process
+    void* comm = nullptr;   // ncclComm_t (real sharding)
+    void* xbuf = nullptr;   // exchange staging buffer (real sharding)
+    size_t xbuf_bytes = 0;
+    std::vector<int> phys;  // logical qubit -> physical bit
+    double* d_scratch = nullptr;
+    size_t scratch_doubles = 0;
+    int device = 0;
+
+    size_t amp_bytes() const { return dbl ? 16 : 8; }
+    uint64_t local_amps() const { return 1ull << nl; }
+    void* shard_ptr(int r) const {  // virtual: shard r; real: own shard
+        return virt ? (void*)((char*)d + (size_t)r * local_amps() * amp_bytes()) : d;
+    }
+};
+
+struct sv_plan_s {
+    svb::Circuit circ;
+    sv_dtype dtype = SV_C64;
+    svb::RunOpts opts;
+    // schedule cache for the identity qubit map on one unsharded GPU
+    bool cached = false;
+    svb::Schedule sched;
+    uint64_t hbm_bytes = 0;
+    cudaGraphExec_t graph = nullptr;
+    void* graph_ptr = nullptr;
+    cudaStream_t graph_stream = nullptr;
+};

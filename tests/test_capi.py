@@ -1,0 +1,64 @@
+"""CPU-side checks of the boundary: libsv.so builds, loads and exports every symbol that
+include/sv.h declares; host-only calls behave (no compute calls without a GPU)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "sv.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sv_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ["sv_create", "sv_apply_gate", "sv_apply_circuit", "sv_probabilities", "sv_amplitudes"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2106_13995_b200 import _lib
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert sorted(_lib.EXPORTED) == declared_symbols()
+
+
+def test_kernels_are_sm100a():
+    """The shared library carries sm_100a SASS (cuobjdump lists the arch)."""
+    import shutil
+    import subprocess
+    from paper_2106_13995_b200 import _lib
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_only_calls():
+    import paper_2106_13995_b200 as P
+    assert P.memory_estimate(42, "c128") == 70368744177664  # P:38 "42-qubit ... 64TB"
+    assert P.memory_estimate(30, "c64") == 8 * 2 ** 30
+    assert P.memory_estimate(61, "c128") == 2 ** 64 - 1     # saturates (R20)
+    from paper_2106_13995_b200._lib import lib
+    assert lib.sv_version().decode().startswith("svb")
+
+
+def test_plan_compile_parse_errors():
+    """IR parse errors name the 1-based line without touching a GPU."""
+    import paper_2106_13995_b200 as P
+    with pytest.raises(P.SvError, match="line 3"):
+        P.Plan("qubits: 3\nH 0\nFOO 1\n")
+    with pytest.raises(P.SvError, match="line 2"):
+        P.Plan("qubits: 3\nCZ 1,1\n")
+    with pytest.raises(P.SvError, match="SV_ERR_PARSE"):
+        P.Plan("H 0\n")
+    p = P.Plan("qubits: 4\nH 0; CNOT 0,1\nU 2 : 1,0,0,0,0,0,1,0\n")
+    assert p.info()["gates"] == 3 and p.info()["n"] == 4

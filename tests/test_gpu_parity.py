@@ -1,0 +1,258 @@
+"""GPU path vs the CPU oracle, element by element, through the C-ABI (libsv.so).
+
+Tolerances (written here): north_star max|d amplitude| <= 1e-10 (c128),
+<= 1e-4 (c64), plus ||d||_2 <= 8 G u (reading R9); bit-exact (==) for basis-input
+permutation circuits (reading R10).  c64 runs feed both sides the c64-rounded input.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import assert_close
+
+pytestmark = pytest.mark.gpu
+
+MODES = {"fused": {}, "per_gate": {"fuse": False}, "dense": {"force_kernel": 2}}
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2106_13995_b200 as P
+    return P
+
+
+def run_gpu(P, text, n, dtype, psi0=None, init=None, **opts):
+    with P.StateVector(n, dtype) as sv:
+        if psi0 is not None:
+            sv.set_amplitudes(psi0)
+        elif init == "uniform":
+            sv.init_uniform()
+        st = sv.apply_circuit(text, **opts)
+        return sv.amplitudes(), st
+
+
+def input_for(n, seed, dtype):
+    psi = W.random_state(n, seed)
+    return W.round_to_c64(psi) if dtype == "c64" else psi
+
+
+# ------------------------------------------------------------------ random circuits, all kinds
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("seed", range(8))
+def test_random_circuits(P, seed, dtype, mode):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 15))
+    c = W.random_circuit(n, 80, seed, max_k=min(5, n), max_controls=2)
+    text = W.to_text(c)
+    psi0 = input_for(n, seed, dtype)
+    got, st = run_gpu(P, text, n, dtype, psi0, **MODES[mode])
+    ref = oracle.simulate(text, psi0)
+    assert st["gates"] == W.gate_count(c)
+    assert_close(got, ref, dtype, W.gate_count(c))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 9, 13, 14, 17])
+def test_every_named_gate_every_position(P, n, dtype):
+    """Each named kind on every qubit (register bits, lane bits, tile bits, tile base bits)."""
+    gates = []
+    rng = np.random.default_rng(n)
+    for name, ar in W.circuits.ARITY.items():
+        if ar > n:
+            continue
+        for q in range(n):
+            qs = [q] + [int(x) for x in rng.choice([p for p in range(n) if p != q], ar - 1, replace=False)]
+            gates.append(W.GateSpec(name, tuple(qs[1:] + qs[:1]) if ar > 1 else (q,)))
+    c = W.Circuit(n, [[g] for g in gates])
+    text = W.to_text(c)
+    psi0 = input_for(n, 100 + n, dtype)
+    ref = oracle.simulate(text, psi0)
+    for mode in MODES.values():
+        got, _ = run_gpu(P, text, n, dtype, psi0, **mode)
+        assert_close(got, ref, dtype, len(gates))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_wide_blocks_and_controls(P, dtype):
+    """U3/U4/U5 blocks with unsorted targets and controls inside and outside the tile."""
+    n = 16
+    rng = np.random.default_rng(5)
+    gates = []
+    for k in (2, 3, 4, 5):
+        for _ in range(4):
+            qs = [int(x) for x in rng.choice(n, k + 2, replace=False)]
+            U = W.circuits.random_unitary(k, rng)
+            gates.append(W.GateSpec("CU", tuple(qs[2:]), tuple(qs[:2]), tuple(complex(x) for x in U.reshape(-1))))
+            gates.append(W.GateSpec("U", tuple(qs[:k]), (), tuple(complex(x) for x in U.conj().T.reshape(-1))))
+    c = W.Circuit(n, [[g] for g in gates])
+    text = W.to_text(c)
+    psi0 = input_for(n, 5, dtype)
+    ref = oracle.simulate(text, psi0)
+    for mode in MODES.values():
+        got, _ = run_gpu(P, text, n, dtype, psi0, **mode)
+        assert_close(got, ref, dtype, len(gates))
+
+
+# ------------------------------------------------------------------ config 1: 12q supremacy d10 c128
+@pytest.mark.parametrize("seed", range(5))
+def test_config1_supremacy_12q(P, seed):
+    c = W.supremacy(4, 3, 10, seed)
+    text = W.to_text(c)
+    ref = oracle.simulate(text)
+    for mode in MODES.values():
+        got, _ = run_gpu(P, text, 12, "c128", **mode)
+        assert_close(got, ref, "c128", W.gate_count(c))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_supremacy_20q_vs_oracle(P, dtype):
+    c = W.supremacy(5, 4, 14, seed=3)
+    text = W.to_text(c)
+    ref = oracle.simulate(text)
+    got, st = run_gpu(P, text, 20, dtype)
+    assert_close(got, ref, dtype, W.gate_count(c))
+    assert st["passes"] < W.gate_count(c) / 4  # fusion really fuses
+
+
+def test_qft_closed_form_gpu(P):
+    n, k = 15, 12345
+    c = W.concat(W.basis_prep(W.Circuit(n, []), k), W.qft(n))
+    got, _ = run_gpu(P, W.to_text(c), n, "c128")
+    j = np.arange(1 << n)
+    expect = np.exp(2j * np.pi * j * k / (1 << n)) / np.sqrt(1 << n)
+    assert np.max(np.abs(got - expect)) <= 1e-12
+
+
+# ------------------------------------------------------------------ config 2: multiplier, basis inputs
+def test_config2_multiplier_21q_bit_exact(P):
+    c = W.multiplier(5)
+    text = W.to_text(c)
+    n = c.n
+    plan = P.Plan(text, "c128")
+    # two full-state comparisons against the oracle, bit for bit
+    for a, b in [(19, 27), (31, 31)]:
+        x = a | (b << 5)
+        psi0 = np.zeros(1 << n, complex)
+        psi0[x] = 1
+        ref = oracle.simulate(text, psi0)
+        with P.StateVector(n, "c128") as sv:
+            sv.init_basis(x)
+            sv.apply_plan(plan)
+            got = sv.amplitudes()
+        assert np.array_equal(got, ref)
+    # all 1024 pairs: amplitude exactly 1 at the oracle's classical image, norm exactly 1
+    ins = np.array([a | (b << 5) for a in range(32) for b in range(32)], dtype=np.uint64)
+    outs = oracle.classical_map(text, ins)
+    with P.StateVector(n, "c128") as sv:
+        for x, y in zip(ins.tolist(), outs.tolist()):
+            sv.init_basis(x)
+            sv.apply_plan(plan)
+            amp = sv.amplitudes(int(y), 1)[0]
+            assert amp == 1 + 0j and sv.norm() == 1.0, (x, y, amp)
+            a, b = x & 31, x >> 5
+            assert y == x | ((a * b) << 10)
+
+
+def test_multiplier_superposition_support(P):
+    """H on A and B: support exactly {|a,b,ab,0>}, each 2^-n (not bit-exact: H rounds)."""
+    nb = 3
+    c = W.multiplier(nb)
+    h = W.Circuit(c.n, [[W.GateSpec("H", (q,)) for q in range(2 * nb)]])
+    got, _ = run_gpu(P, W.to_text(W.concat(h, c)), c.n, "c128")
+    expect = np.zeros(1 << c.n)
+    for a in range(1 << nb):
+        for b in range(1 << nb):
+            expect[a | (b << nb) | ((a * b) << (2 * nb))] = 2.0 ** -nb
+    assert np.max(np.abs(got - expect)) <= 1e-12
+
+
+# ------------------------------------------------------------------ readout / init
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_readout_probabilities_norm(P, dtype):
+    n = 14
+    c = W.supremacy(4, 3, 6, seed=1)
+    c = W.Circuit(n, c.moments + [[W.GateSpec("H", (12,)), W.GateSpec("SqrtX", (13,))]])
+    text = W.to_text(c)
+    psi0 = input_for(n, 7, dtype)
+    ref = oracle.simulate(text, psi0)
+    with P.StateVector(n, dtype) as sv:
+        sv.set_amplitudes(psi0)
+        sv.apply_circuit(text)
+        tol = 1e-12 if dtype == "c128" else 1e-5
+        for qs in ([], [0], [13], [3, 0, 11], list(range(n)), [5, 6, 7, 8, 9, 10, 1]):
+            got = sv.probabilities(qs)
+            assert np.max(np.abs(got - oracle.probabilities(ref, qs))) <= tol, qs
+        assert abs(sv.norm() - oracle.norm(ref)) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_init_states(P, dtype):
+    for n in (1, 7, 20):
+        with P.StateVector(n, dtype) as sv:
+            a = sv.amplitudes()
+            assert a[0] == 1 and np.count_nonzero(a) == 1
+            sv.init_uniform()
+            u = oracle.uniform_state(n)
+            if dtype == "c64":
+                u = W.round_to_c64(u)
+            assert np.array_equal(sv.amplitudes().astype(complex), u)
+            k = (1 << n) - 1 - (n // 3)
+            sv.init_basis(k)
+            a = sv.amplitudes()
+            assert a[k] == 1 and np.count_nonzero(a) == 1
+
+
+def test_apply_gate_api(P):
+    n = 9
+    rng = np.random.default_rng(2)
+    psi0 = W.random_state(n, 2)
+    U = W.circuits.random_unitary(2, rng)
+    with P.StateVector(n, "c128") as sv:
+        sv.set_amplitudes(psi0)
+        sv.apply_gate(U, [7, 2], [4])
+        got = sv.amplitudes()
+    ref = oracle.apply_gate(psi0.copy(), U, [7, 2], [4])
+    assert np.max(np.abs(got - ref)) <= 1e-13
+    with P.StateVector(n, "c128") as sv:
+        with pytest.raises(P.SvError, match="SV_ERR_RANGE"):
+            sv.apply_gate(np.eye(2), [9])
+        with pytest.raises(P.SvError, match="SV_ERR_RANGE"):
+            sv.apply_gate(np.eye(4), [1, 1])
+        with pytest.raises(P.SvError, match="SV_ERR_ARG"):
+            sv.apply_gate(np.eye(64), [0, 1, 2, 3, 4, 5])
+
+
+def test_empty_circuit_and_identity(P):
+    psi0 = W.random_state(6, 4)
+    got, st = run_gpu(P, "qubits: 6\n", 6, "c128", psi0)
+    assert np.array_equal(got, psi0) and st["passes"] == 0
+    eye = ",".join("1.0,0.0" if r == c else "0.0,0.0" for r in range(4) for c in range(4))
+    got, _ = run_gpu(P, f"qubits: 6\nU 5,2 : {eye}\n", 6, "c128", psi0)
+    assert np.array_equal(got, psi0)  # identity Custom gate, exact
+
+
+def test_determinism_bitwise(P):
+    c = W.supremacy(5, 4, 10, seed=8)
+    text = W.to_text(c)
+    a, _ = run_gpu(P, text, 20, "c64")
+    b, _ = run_gpu(P, text, 20, "c64")
+    assert np.array_equal(a, b)
+    with P.StateVector(20, "c64") as sv:
+        sv.apply_circuit(text)
+        n1 = sv.norm()
+        assert all(sv.norm() == n1 for _ in range(3))
+
+
+def test_cuda_graph_replay(P):
+    c = W.supremacy(4, 4, 8, seed=2)
+    text = W.to_text(c)
+    ref = oracle.simulate(text)
+    plan = P.Plan(text, "c128", use_graph=True)
+    with P.StateVector(16, "c128") as sv:
+        for _ in range(3):
+            sv.init_zero()
+            sv.apply_plan(plan)
+            assert_close(sv.amplitudes(), ref, "c128", W.gate_count(c))
