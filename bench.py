@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""bench.py -- gates/s and circuit wall time of the state-vector hot path on B200.
+
+Metric (BASELINE.json): "gates/s and circuit wall time at 30q; achieved HBM GB/s vs peak at
+1/2/4/8 B200".  One step = one pass of the whole hot path (SURVEY 8(a) a3+a4: initialise
+|0...0> in HBM and apply every gate of the circuit through its fused tile passes; the plan
+is compiled once, outside the timed region, reading R13 T_run).
+
+  N = 1 : 30-qubit supremacy-style circuit, 6x5 grid, 20 cycles, 507 gates (BASELINE config 3),
+          complex64 by default (--dtype c128 for the other half of config 3).
+  N > 1 : weak scaling, 2^30 amplitudes per GPU: a (30 + log2 N)-qubit supremacy circuit on a
+          7x5 grid (first n sites) sharded by its top log2 N qubits, global<->local swaps over
+          NCCL.  value = N * gates / step time ("shard-gates/s": every rank applies every gate
+          to its 2^30-amplitude shard).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype c64|c128]
+                       [--workload supremacy|multiplier] [--impl ours|reference]
+Under torchrun (N > 1) every rank runs; rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "gates/s and circuit wall time at 30q; achieved HBM GB/s vs peak at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--workload", default="supremacy", choices=["supremacy", "multiplier"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--qubits", type=int, default=30, help="qubits per GPU (default 30)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+def make_workload(args, world: int):
+    import workloads as W
+    g = world.bit_length() - 1
+    n = args.qubits + g
+    if args.workload == "supremacy":
+        if n == 30:
+            c = W.supremacy(6, 5, 20, seed=0)
+            name = "supremacy 6x5 grid, 20 cycles, seed 0"
+        else:
+            rows = (n + 4) // 5
+            c = W.supremacy(rows, 5, 20, seed=0, n=n)
+            name = f"supremacy {rows}x5 grid (first {n} sites), 20 cycles, seed 0"
+    else:
+        # 31q multiplier (BASELINE config 4): rectangular 8x7 (reading R7), basis-free uniform input
+        if n != 31:
+            raise SystemExit("--workload multiplier is defined for 31 qubits (use --qubits 31)")
+        c = W.multiplier(8, 7)
+        name = "multiplier 8x7 (shift-and-add Cuccaro), 455 gates"
+    return c, W.to_text(c), name
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ peaks / profiles
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profiled_traffic(dtype: str):
+    """Per-launch dram bytes of the tile-pass kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(dtype)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def cpu_baseline(text: str, n: int, budget_s: float):
+    """The oracle as it stands (fp64, all host cores) on a bounded sample: gates [k0, k0+m) of the
+    same circuit at the same width, m chosen so the sample takes about budget_s seconds."""
+    import numpy as np
+    import oracle
+    mem_needed = 16 << n
+    try:
+        avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    except Exception:
+        avail = 0
+    n_eff = n
+    note = ""
+    while mem_needed > 0.6 * avail and n_eff > 20:
+        n_eff -= 1
+        mem_needed //= 2
+    if n_eff != n:
+        note = f" (host RAM {avail >> 30} GiB: sampled at {n_eff} qubits, time scaled by 2^{n - n_eff})"
+    psi = np.zeros(1 << n_eff, dtype=np.complex128)
+    psi[0] = 1
+    ntot = oracle.circuit_info(text)[1]
+    if n_eff != n:
+        # same circuit family at the reduced width: drop qubits >= n_eff and their gates
+        lines = []
+        for ln in text.splitlines():
+            if ln.startswith("qubits:"):
+                lines.append(f"qubits: {n_eff}")
+                continue
+            if ":" in ln and not ln.startswith(("U", "CU")) and (ln.startswith("family") or ln.startswith("meta")):
+                lines.append(ln)
+                continue
+            keep = []
+            for g in ln.split(";"):
+                g = g.strip()
+                if not g:
+                    continue
+                qs = [int(x) for x in g.split()[1].split(",")]
+                if max(qs) < n_eff:
+                    keep.append(g)
+            if keep:
+                lines.append("; ".join(keep))
+        text = "\n".join(lines) + "\n"
+        ntot = oracle.circuit_info(text)[1]
+    k0 = min(n_eff, ntot - 1)  # past the H layer: the mixed body of the circuit
+    t0 = time.perf_counter()
+    oracle.run(text, psi, first=k0, count=1)
+    one = time.perf_counter() - t0
+    m = max(1, min(ntot - k0 - 1, int(budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.run(text, psi, first=k0 + 1, count=m)
+    dt = time.perf_counter() - t0
+    rate = m / dt / (2 ** (n - n_eff))
+    return {"value": rate, "unit": "gates/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{m} consecutive gates (from gate {k0 + 1}) of the same circuit at {n_eff} qubits, "
+                      f"complex128, {dt:.1f} s{note}"}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    c, text, name = make_workload(args, 1)
+    n = c.n
+    avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    n_eff = n
+    while (16 << n_eff) > 0.6 * avail and n_eff > 20:
+        n_eff -= 1
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    per = []
+    psi = None
+    G = oracle.circuit_info(text)[1]
+    if n_eff == n:
+        psi = np.zeros(1 << n, dtype=np.complex128)
+        psi[0] = 1
+        t0 = time.perf_counter()
+        oracle.run(text, psi, first=n, count=1)
+        one = time.perf_counter() - t0
+        m = max(1, int(budget / max(one, 1e-6)))
+        k = n + 1
+        for s in range(args.warmup + args.steps):
+            cnt = min(m, G - k) if G - k > 0 else m
+            if G - k <= 0:
+                k = n
+            t0 = time.perf_counter()
+            oracle.run(text, psi, first=k, count=cnt)
+            dt = time.perf_counter() - t0
+            k += cnt
+            if s >= args.warmup:
+                per.append((cnt, dt))
+        gates = sum(x for x, _ in per)
+        secs = sum(y for _, y in per)
+        value = gates / secs
+        sample = f"{m} gates per step of the {n}-qubit circuit, complex128 oracle"
+    else:
+        cb = cpu_baseline(text, n, budget)
+        value = cb["value"]
+        secs = 0.0
+        sample = cb["sample"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": (secs / max(1, args.steps)) * 1e3 if secs else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": name, "n_qubits": n, "gates": G},
+            "cpu_baseline": {"value": value, "unit": "gates/s", "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2106_13995_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c, text, name = make_workload(args, world)
+    n = c.n
+    G = len(c.gates)
+    if world > 1:
+        sv = P.StateVector.sharded(n, args.dtype)
+    else:
+        sv = P.StateVector(n, args.dtype)
+    stream = torch.cuda.ExternalStream(sv.stream_ptr())
+    plan = P.Plan(text, args.dtype)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also compiles + caches the schedule)
+    st = None
+    for _ in range(args.warmup):
+        sv.init_zero()
+        st = sv.apply_plan(plan)
+    sv.sync()
+    passes = st["passes"] if st else 0
+    info = plan.info()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    clk.start()
+    barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    for i in range(args.steps):
+        e0, e1, e2 = ev[i]
+        e0.record(stream)
+        sv.init_zero()
+        e1.record(stream)
+        st = sv.apply_plan(plan)
+        e2.record(stream)
+    sv.sync()
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - t_wall
+    clocks = clk.stop()
+    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
+    pass_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev]
+    total_ms = sum(step_ms)
+    tpass_ms = sum(pass_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, tpass_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, tpass_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = world * G / (ms_per_step / 1e3)
+    amp = 16 if args.dtype == "c128" else 8
+    local_amps = 1 << (n - (world.bit_length() - 1))
+    bytes_per_launch = 2 * local_amps * amp
+    launches = max(1, st["launches"])
+    avg_launch_ms = tpass_ms / (args.steps * launches)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+
+    # e2e: same metric through the public API with host buffers: IR text in, parse + plan +
+    # init + apply, marginal probabilities of 20 qubits (8 MiB fp64) back to the host.
+    e2e_q = list(range(min(20, n)))
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sv.init_zero()
+        sv.apply_circuit(text)
+        probs = sv.probabilities(e2e_q)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    assert abs(probs.sum() - 1.0) < 1e-3
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(text, n, args.cpu_seconds)
+        except Exception as e:  # report, never hide
+            cpu = {"value": None, "unit": "gates/s", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "gates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": args.dtype,
+            "data": "synthetic",
+            "config": {
+                "workload": name,
+                "n_qubits": n,
+                "n_qubits_per_gpu": n - (world.bit_length() - 1),
+                "gates": G,
+                "passes_per_step": passes,
+                "stages_per_step": info.get("stages"),
+                "swaps_per_step": st.get("swaps", 0),
+                "state_bytes_per_gpu": local_amps * amp,
+                "timed": "init |0...0> + all tile passes (plan compiled once, outside the timed region)",
+                "l2": "state (>= 8 GiB per GPU) is larger than L2 (126 MB): no flush needed",
+                "parallelism": f"sharded by top {world.bit_length() - 1} qubits" if world > 1 else "single GPU",
+            },
+            "circuit_wall_ms": ms_per_step,
+            "hbm_gbs": achieved,
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "tile_pass_kernel",
+                "achieved": achieved,
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": profiled_traffic(args.dtype),
+                "bytes_per_launch": bytes_per_launch,
+                "avg_launch_ms": avg_launch_ms,
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * G / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": len(text.encode()),
+                    "d2h_bytes_per_step": 8 * len(probs),
+                    "includes": "IR text parse + plan + init + passes + 20-qubit marginal D2H"},
+            "gpu_launches": int(args.steps * launches),
+            "clocks": clocks,
+            "wall_s_timed_region": wall,
+        }
+        print(json.dumps(line), flush=True)
+    sv.close()
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

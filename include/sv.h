@@ -63,9 +63,10 @@ typedef enum {
 
 /* Kernel selection for ablations (sv_run_opts.force_kernel). */
 typedef enum {
-    SV_KERNEL_AUTO = 0,       /* fused multi-stage tile passes (default) */
-    SV_KERNEL_PER_GATE = 1,   /* one single-stage pass per gate (no fusion)  */
-    SV_KERNEL_DENSE = 2       /* one pass per gate, every gate as a generic dense block */
+    SV_KERNEL_AUTO = 0,       /* fused tile passes, each compiled to a specialised sm_100a kernel (default) */
+    SV_KERNEL_PER_GATE = 1,   /* one single-stage pass per gate (no fusion), precompiled interpreter kernel */
+    SV_KERNEL_DENSE = 2,      /* one pass per gate, every gate as a generic dense block (K4) */
+    SV_KERNEL_INTERP = 3      /* fused tile passes run by the precompiled interpreter kernel (ablation) */
 } sv_kernel;
 
 typedef struct {
@@ -139,6 +140,10 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
 sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts* opts,
                           sv_plan* out);
 sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uint64_t* stages);
+/* Generated CUDA source of tile pass `pass` of the single-GPU schedule (inspection and
+ * profiling).  Writes at most cap bytes (NUL-terminated) and the full length to *len.
+ * Returns SV_ERR_RANGE for a bad pass index; an empty string for a non-tile pass. */
+sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len);
 sv_status sv_plan_destroy(sv_plan p);
 
 /* Apply a compiled plan to a state (asynchronous).  stats may be NULL. */

@@ -1,6 +1,6 @@
 """Build libsv.so in-tree: nvcc for sm_100a (-gencode arch=compute_100a,code=sm_100a -lineinfo).
 
-Usage: python -m paper_2106_13995_b200.build [--force] [--verbose]
+Usage: python paper_2106_13995_b200/build.py [--force] [--verbose]
 """
 
 from __future__ import annotations
@@ -30,8 +30,9 @@ def nccl_dirs():
     raise RuntimeError("NCCL (nvidia-nccl wheel) not found; needed for the sharded layer")
 
 
-SOURCES = ["kernels.cu", "ir.cpp", "planner.cpp", "capi.cpp", "sharded.cpp", "comm.cpp"]
-HEADERS = ["sv_internal.hpp", "sv_kernels.hpp", "engine.hpp", "state.hpp", "comm.hpp"]
+SOURCES = ["kernels.cu", "ir.cpp", "planner.cpp", "capi.cpp", "sharded.cpp", "comm.cpp", "jit.cpp"]
+HEADERS = ["sv_internal.hpp", "sv_kernels.hpp", "engine.hpp", "state.hpp", "comm.hpp", "jit.hpp"]
+CUDA_LIB = "/usr/local/cuda/lib64"
 
 
 def _newest_header():
@@ -66,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, inc, verbose, force), SOURCES))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L" + libdir, "-l:libnccl.so.2",
-               "-Xlinker", "-rpath=" + libdir]
+               "-L" + CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + libdir + ":" + CUDA_LIB]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "comm.hpp"
+#include "jit.hpp"
 #include "state.hpp"
 
 using namespace svb;
@@ -128,7 +129,9 @@ int shard_rank(const sv_state_s* s, int i) { return s->virt ? i : s->rank; }
 sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stats* st) {
     for (const PassPlan& pp : sc.passes) {
         cudaError_t e;
-        if (pp.kind == PassPlan::TILE)
+        if (pp.kind == PassPlan::TILE && pp.jit_fn)
+            e = jit_launch(pp, psi, s->stream);
+        else if (pp.kind == PassPlan::TILE)
             e = launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles, s->stream);
         else
             e = launch_dense_k(s->dbl, psi, pp.params.data(), pp.groups, s->stream);
@@ -140,6 +143,28 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
             st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
         }
     }
+    return SV_OK;
+}
+
+// Single-GPU schedule of a plan (identity qubit map): lower every gate, fuse, plan passes.
+sv_status plan_schedule(sv_plan_s* p) {
+    Context ctx;
+    ctx.n = ctx.nl = p->circ.n;
+    ctx.phys.resize(p->circ.n);
+    for (int q = 0; q < p->circ.n; ++q) ctx.phys[q] = q;
+    ctx.dbl = p->dtype == SV_C128;
+    std::string err;
+    std::vector<LOp> ops;
+    for (size_t i = 0; i < p->circ.gates.size(); ++i) {
+        bool needs_global = false;
+        const sv_status st = lower_gate(p->circ.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
+        if (st != SV_OK) return fail(st, err);
+    }
+    p->sched = Schedule();
+    const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err);
+    if (st != SV_OK) return fail(st, err);
+    p->cached = true;
+    p->jitted = false;
     return SV_OK;
 }
 
@@ -369,7 +394,7 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
 sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts* opts, sv_plan* out) {
     if (!out || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
     if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
-    if (opts && (opts->force_kernel < 0 || opts->force_kernel > 2 || opts->tile_qubits < 0))
+    if (opts && (opts->force_kernel < 0 || opts->force_kernel > 3 || opts->tile_qubits < 0))
         return fail(SV_ERR_ARG, "bad sv_run_opts");
     auto* p = new sv_plan_s();
     std::string err;
@@ -380,6 +405,11 @@ sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts
     }
     p->dtype = dtype;
     p->opts = to_opts(opts);
+    const sv_status s2 = plan_schedule(p);
+    if (s2 != SV_OK) {
+        delete p;
+        return s2;
+    }
     *out = p;
     return SV_OK;
 }
@@ -390,6 +420,25 @@ sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uin
     if (gates) *gates = p->circ.gates.size();
     if (passes) *passes = p->cached ? p->sched.passes.size() : 0;
     if (stages) *stages = p->cached ? p->sched.stages : 0;
+    return SV_OK;
+}
+
+sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len) {
+    if (!p) return fail(SV_ERR_ARG, "NULL plan");
+    if (!p->cached || pass < 0 || pass >= (int)p->sched.passes.size()) return fail(SV_ERR_RANGE, "bad pass index");
+    const PassPlan& pp = p->sched.passes[pass];
+    std::string src;
+    if (pp.kind == PassPlan::TILE && pp.sym) {
+        int threads;
+        size_t smem;
+        src = gen_pass_source(*pp.sym, threads, smem);
+    }
+    if (len) *len = src.size();
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, src.size());
+        memcpy(buf, src.data(), n);
+        buf[n] = 0;
+    }
     return SV_OK;
 }
 
@@ -408,16 +457,13 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
     if (s->world > 1) return sharded_apply(s, p, stats);
     std::string err;
     if (!p->cached) {
-        const Context ctx = ctx_of(s, 0);
-        std::vector<LOp> ops;
-        for (size_t i = 0; i < p->circ.gates.size(); ++i) {
-            bool needs_global = false;
-            const sv_status st = lower_gate(p->circ.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
-            if (st != SV_OK) return fail(st, err);
-        }
-        const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err);
+        const sv_status st = plan_schedule(p);
+        if (st != SV_OK) return st;
+    }
+    if (!p->jitted && p->opts.use_jit()) {
+        const sv_status st = jit_prepare(p->sched, err);
         if (st != SV_OK) return fail(st, err);
-        p->cached = true;
+        p->jitted = true;
     }
     sv_status st = SV_OK;
     if (p->opts.use_graph) {

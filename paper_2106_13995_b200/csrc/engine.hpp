@@ -63,6 +63,7 @@ struct RunOpts {
     int force_kernel = SV_KERNEL_AUTO;
     bool check_unitary = false;
     bool use_graph = false;
+    bool use_jit() const { return fuse && force_kernel == SV_KERNEL_AUTO; }
 };
 
 // Lower one gate to ops on physical local qubits; folds global qubits (rank constants).
@@ -71,8 +72,24 @@ sv_status lower_gate(const Gate& g, int gi, const Context& ctx, const RunOpts& o
                      bool& needs_global, std::string& err);
 
 // ------------------------------------------------------------------ schedule
+struct StageSym {
+    std::vector<int> rq;         // physical qubit of register bit j (size rb)
+    std::vector<LOp> ops;        // in application order
+};
+
+struct TileSym {                 // symbolic tile pass: what both backends execute
+    std::vector<int> tq;         // tile qubits, ascending
+    int rb = 0;
+    bool dbl = false;
+    std::vector<StageSym> stages;
+};
+
 struct PassPlan {
     enum Kind { TILE, DENSE } kind = TILE;
+    std::shared_ptr<TileSym> sym;        // TILE: the symbolic pass
+    void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
+    int jit_threads = 0;
+    size_t jit_smem = 0;
     int rb = 0, m = 0, nstages = 0;
     uint64_t ntiles = 0, groups = 0;
     int nops = 0;

@@ -1,0 +1,469 @@
+// jit.cpp -- per-pass specialised sm_100a kernels (the workhorse).
+//
+// The interpreter kernel (kernels.cu) dispatches every op at run time; measured on B200 it
+// is instruction-cache bound (1 MB of SASS, ~60% "no_instructions" stalls; profiles/).  Here
+// each fused tile pass is emitted as straight-line CUDA from a fixed template and compiled
+// once with NVRTC for sm_100a:
+//   * register positions of every op are compile-time constants, so X / SWAP / Y are
+//     register renames and the butterflies of H, SqrtX, SqrtY (and inverses) are 4 FADD per
+//     amplitude pair: their scalar factors (1/sqrt2, (1 +- i)/2) are deferred and applied
+//     once at the end of the pass (SURVEY 8(d) "specialised arithmetic");
+//   * matrix entries are immediates; exact 0 entries are skipped and exact 1 entries are
+//     moves, so permutation gates move data without floating point (reading R10);
+//   * controls on register bits select amplitudes at compile time; controls and diagonal
+//     factors on other bits are predicates on the amplitude index (reading a4').
+// Modules are cached in-process by source text (plan cache, SURVEY 8(b) sv_run_opts).
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+
+#include "jit.hpp"
+
+namespace svb {
+
+namespace {
+
+struct Em {
+    std::ostringstream o;
+    bool dbl = false;
+
+    std::string lit(double v) const {
+        char b[64];
+        if (dbl) {
+            snprintf(b, sizeof b, "%a", v);
+            return std::string("(") + b + ")";
+        }
+        const float f = (float)v;
+        snprintf(b, sizeof b, "%a", (double)f);
+        return std::string("(") + b + "f)";
+    }
+};
+
+bool is1(const cd& c) { return c == cd(1, 0); }
+bool is0(const cd& c) { return c == cd(0, 0); }
+
+// (re, im) expressions of var * c, exact for 0, +-1, +-i
+std::pair<std::string, std::string> mul(const Em& e, const std::string& v, const cd& c) {
+    const double cr = c.real(), ci = c.imag();
+    const std::string x = v + ".x", y = v + ".y";
+    if (ci == 0.0) {
+        if (cr == 1.0) return {x, y};
+        if (cr == -1.0) return {"(-" + x + ")", "(-" + y + ")"};
+        return {x + "*" + e.lit(cr), y + "*" + e.lit(cr)};
+    }
+    if (cr == 0.0) {
+        if (ci == 1.0) return {"(-" + y + ")", x};
+        if (ci == -1.0) return {y, "(-" + x + ")"};
+        return {"(-" + y + ")*" + e.lit(ci), x + "*" + e.lit(ci)};
+    }
+    if (cr == ci) return {"(" + x + "-" + y + ")*" + e.lit(cr), "(" + x + "+" + y + ")*" + e.lit(cr)};
+    if (cr == -ci) return {"(" + x + "+" + y + ")*" + e.lit(cr), "(" + y + "-" + x + ")*" + e.lit(cr)};
+    return {x + "*" + e.lit(cr) + "-" + y + "*" + e.lit(ci), x + "*" + e.lit(ci) + "+" + y + "*" + e.lit(cr)};
+}
+
+std::string reg(int s) { return "v[" + std::to_string(s) + "]"; }
+
+// out_r = sum_c M[r][c] in_c for a d x d matrix over registers idx[0..d-1]
+void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M) {
+    const size_t d = idx.size();
+    e.o << "{";
+    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+    for (size_t r = 0; r < d; ++r) {
+        std::string re, im;
+        for (size_t c = 0; c < d; ++c) {
+            const cd m = M[r * d + c];
+            if (is0(m)) continue;
+            auto p = mul(e, "i" + std::to_string(c), m);
+            re += (re.empty() ? "" : "+") + p.first;
+            im += (im.empty() ? "" : "+") + p.second;
+        }
+        if (re.empty()) { re = e.lit(0.0); im = e.lit(0.0); }
+        e.o << reg(idx[r]) << "=mk(" << re << "," << im << ");";
+    }
+    e.o << "}\n";
+}
+
+// unscaled form M' and deferred factor f with U = f M' (no controls only)
+bool unscaled(int kind, std::vector<cd>& M, cd& f) {
+    const cd I(0, 1);
+    const double r = 0.70710678118654752440;
+    switch (kind) {
+        case OP_H: M = {1, 1, 1, -1}; f = r; return true;
+        case OP_SX: M = {1, -I, -I, 1}; f = cd(.5, .5); return true;
+        case OP_SXDG: M = {1, I, I, 1}; f = cd(.5, -.5); return true;
+        case OP_SY: M = {1, -1, 1, 1}; f = cd(.5, .5); return true;
+        case OP_SYDG: M = {1, 1, -1, 1}; f = cd(.5, -.5); return true;
+        case OP_X: M = {0, 1, 1, 0}; f = 1; return true;
+        case OP_Y: M = {0, -I, I, 0}; f = 1; return true;
+        default: return false;
+    }
+}
+
+cd diag_const(int kind) {
+    const double r = 0.70710678118654752440;
+    switch (kind) {
+        case OP_Z: return -1;
+        case OP_S: return cd(0, 1);
+        case OP_SDG: return cd(0, -1);
+        case OP_T: return cd(r, r);
+        case OP_TDG: return cd(r, -r);
+        default: return 1;
+    }
+}
+
+struct StageCtx {
+    int rb;
+    int pos[64];  // physical qubit -> register position, -1 if not a register bit
+};
+
+void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
+    const int R = 1 << sc.rb;
+    uint32_t creg = 0;
+    uint64_t cm = 0;
+    for (int c : op.ctrl) {
+        if (sc.pos[c] >= 0) creg |= 1u << sc.pos[c];
+        else cm |= 1ull << c;
+    }
+    const bool controlled = !op.ctrl.empty();
+    if (cm) e.o << "if((g&" << cm << "ull)==" << cm << "ull){\n";
+    auto sel = [&](int s) { return (s & creg) == creg; };
+    const int k = (int)op.tq.size();
+    std::vector<int> p(k);
+    for (int j = 0; j < k; ++j) p[j] = sc.pos[op.tq[j]];
+    switch (op.kind) {
+        case OP_U1: case OP_H: case OP_SX: case OP_SXDG: case OP_SY: case OP_SYDG: case OP_X: case OP_Y:
+        case OP_U2: case OP_U3: case OP_U4: case OP_SWAP: {
+            std::vector<cd> M;
+            cd f = 1;
+            if (op.kind == OP_U1 || op.kind == OP_U2 || op.kind == OP_U3 || op.kind == OP_U4) {
+                M = op.coef;
+            } else if (op.kind == OP_SWAP) {
+                M = {1, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 0, 1};
+            } else {
+                unscaled(op.kind, M, f);
+                if (controlled) {
+                    for (cd& x : M) x *= f;
+                    f = 1;
+                }
+            }
+            fac *= f;
+            uint32_t tmask = 0;
+            for (int j = 0; j < k; ++j) tmask |= 1u << p[j];
+            const int d = 1 << k;
+            for (int s = 0; s < R; ++s) {
+                if (s & tmask) continue;
+                if (!sel(s)) continue;
+                std::vector<int> idx(d);
+                for (int c = 0; c < d; ++c) {
+                    int x = s;
+                    for (int j = 0; j < k; ++j)
+                        if ((c >> j) & 1) x |= 1 << p[j];
+                    idx[c] = x;
+                }
+                if (op.kind == OP_SWAP || op.kind == OP_X) {
+                    // pure register permutation: M[r][c] == 1 at one c per row
+                    e.o << "{";
+                    for (int c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+                    for (int r = 0; r < d; ++r)
+                        for (int c = 0; c < d; ++c)
+                            if (is1(M[r * d + c])) e.o << reg(idx[r]) << "=i" << c << ";";
+                    e.o << "}\n";
+                } else {
+                    emit_dense(e, idx, M);
+                }
+            }
+        } break;
+        case OP_PHASE: case OP_DIAG1: case OP_Z: case OP_S: case OP_SDG: case OP_T: case OP_TDG:
+        case OP_SCALAR: {
+            cd c0 = 1, c1 = 1;
+            if (op.kind == OP_DIAG1) { c0 = op.coef[0]; c1 = op.coef[1]; }
+            else if (op.kind == OP_PHASE) c1 = op.coef[0];
+            else if (op.kind == OP_SCALAR) { c0 = op.coef[0]; c1 = op.coef[0]; }
+            else c1 = diag_const(op.kind);
+            const int q = op.dq.empty() ? -1 : op.dq[0];
+            const int pq = q >= 0 ? sc.pos[q] : -1;
+            if (q >= 0 && pq < 0) {
+                // factor chosen by an index bit that is not a register bit
+                e.o << "{const bool b=((g>>" << q << ")&1ull)!=0;";
+                for (int br = 0; br < 2; ++br) {
+                    const cd c = br ? c1 : c0;
+                    if (is1(c)) continue;
+                    e.o << (br ? "if(b){" : "if(!b){");
+                    for (int s = 0; s < R; ++s) {
+                        if (!sel(s)) continue;
+                        auto m = mul(e, reg(s), c);
+                        e.o << reg(s) << "=mk(" << m.first << "," << m.second << ");";
+                    }
+                    e.o << "}";
+                }
+                e.o << "}\n";
+            } else {
+                for (int s = 0; s < R; ++s) {
+                    if (!sel(s)) continue;
+                    const cd c = (pq < 0) ? c0 : (((s >> pq) & 1) ? c1 : c0);
+                    if (is1(c)) continue;
+                    auto m = mul(e, reg(s), c);
+                    e.o << reg(s) << "=mk(" << m.first << "," << m.second << ");";
+                }
+                e.o << "\n";
+            }
+        } break;
+        case OP_DIAG2: {
+            const int q0 = op.dq[0], q1 = op.dq[1];
+            const int p0 = sc.pos[q0], p1 = sc.pos[q1];
+            // runtime bits: enumerate their combinations
+            std::vector<int> rtq;
+            if (p0 < 0) rtq.push_back(q0);
+            if (p1 < 0) rtq.push_back(q1);
+            e.o << "{";
+            for (size_t j = 0; j < rtq.size(); ++j) e.o << "const int b" << j << "=(int)((g>>" << rtq[j] << ")&1ull);";
+            for (int combo = 0; combo < (1 << rtq.size()); ++combo) {
+                if (!rtq.empty()) {
+                    e.o << "if(";
+                    for (size_t j = 0; j < rtq.size(); ++j) e.o << (j ? "&&" : "") << "b" << j << "==" << ((combo >> j) & 1);
+                    e.o << "){";
+                }
+                for (int s = 0; s < R; ++s) {
+                    if (!sel(s)) continue;
+                    int ri = 0, bi0, bi1;
+                    if (p0 >= 0) bi0 = (s >> p0) & 1; else bi0 = (combo >> ri++) & 1;
+                    if (p1 >= 0) bi1 = (s >> p1) & 1; else bi1 = (combo >> ri++) & 1;
+                    const cd c = op.coef[bi0 | (bi1 << 1)];
+                    if (is1(c)) continue;
+                    auto m = mul(e, reg(s), c);
+                    e.o << reg(s) << "=mk(" << m.first << "," << m.second << ");";
+                }
+                if (!rtq.empty()) e.o << "}";
+            }
+            e.o << "}\n";
+        } break;
+        default:
+            break;
+    }
+    if (cm) e.o << "}\n";
+}
+
+uint32_t swz_const(uint32_t x, bool dbl) { return swizzle_slot(x, dbl ? 3 : 4); }
+
+// run-length emission of  sum_i ((t >> i) & 1) << dst[i]
+std::string deposit_expr(const std::vector<int>& dst, bool wide) {
+    std::string ex;
+    const std::string cast = wide ? "(unsigned long long)" : "(unsigned)";
+    size_t i = 0;
+    while (i < dst.size()) {
+        size_t j = i + 1;
+        while (j < dst.size() && dst[j] - (int)j == dst[i] - (int)i) ++j;
+        const uint32_t mask = (((1u << (j - i)) - 1) << i);
+        const int shift = dst[i] - (int)i;
+        std::ostringstream t;
+        t << "(" << cast << "(t&" << mask << "u)";
+        if (shift > 0) t << "<<" << shift;
+        else if (shift < 0) t << ">>" << -shift;
+        t << ")";
+        ex += (ex.empty() ? "" : "|") + t.str();
+        i = j;
+    }
+    return ex.empty() ? (wide ? "0ull" : "0u") : ex;
+}
+
+}  // namespace
+
+std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
+    Em e;
+    e.dbl = sym.dbl;
+    const int rb = sym.rb, R = 1 << rb;
+    const int m = (int)sym.tq.size();
+    const int tb = m - rb;
+    threads = 1 << tb;
+    const bool multi = sym.stages.size() > 1;
+    smem = multi ? ((size_t)1 << m) * (sym.dbl ? 16 : 8) : 0;
+    int local_of[64];
+    for (int i = 0; i < 64; ++i) local_of[i] = -1;
+    for (int b = 0; b < m; ++b) local_of[sym.tq[b]] = b;
+
+    auto& o = e.o;
+    o << "// generated tile pass: m=" << m << " rb=" << rb << " stages=" << sym.stages.size() << "\n";
+    o << "typedef " << (sym.dbl ? "double" : "float") << " R;\n";
+    o << "struct alignas(" << (sym.dbl ? 16 : 8) << ") C { R x, y; };\n";
+    o << "__device__ __forceinline__ C mk(R x, R y){C c; c.x=x; c.y=y; return c;}\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << "," << (threads >= 256 ? 2 : 4)
+      << ") svpass(C* __restrict__ psi){\n";
+    if (multi) o << "extern __shared__ C sm[];\n";
+    o << "const unsigned t=threadIdx.x;\n";
+    o << "unsigned long long base=blockIdx.x;\n";
+    for (int b = 0; b < m; ++b) {
+        const int q = sym.tq[b];
+        o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
+    }
+    o << "C v[" << R << "];\nunsigned long long g;\n";
+    if (multi) o << "unsigned tl;\n";
+    cd fac = 1;
+    for (size_t si = 0; si < sym.stages.size(); ++si) {
+        const StageSym& st = sym.stages[si];
+        StageCtx sc;
+        sc.rb = rb;
+        for (int i = 0; i < 64; ++i) sc.pos[i] = -1;
+        for (int j = 0; j < rb; ++j) sc.pos[st.rq[j]] = j;
+        std::vector<int> tq_phys, tq_local;
+        for (int b = 0; b < m; ++b)
+            if (sc.pos[sym.tq[b]] < 0) { tq_phys.push_back(sym.tq[b]); tq_local.push_back(b); }
+        o << "// stage " << si << ": registers";
+        for (int q : st.rq) o << " " << q;
+        o << "\n";
+        o << "g=base|" << deposit_expr(tq_phys, true) << ";\n";
+        std::vector<uint64_t> goff(R);
+        std::vector<uint32_t> loff(R);
+        for (int s = 0; s < R; ++s) {
+            uint64_t go = 0;
+            uint32_t lo = 0;
+            for (int j = 0; j < rb; ++j)
+                if ((s >> j) & 1) { go |= 1ull << st.rq[j]; lo |= 1u << local_of[st.rq[j]]; }
+            goff[s] = go;
+            loff[s] = swz_const(lo, sym.dbl);
+        }
+        if (multi) {
+            const std::string tl = deposit_expr(tq_local, false);
+            const int lb = sym.dbl ? 3 : 4;
+            o << "tl=" << tl << ";\n";
+            o << "{unsigned y=tl>>" << lb << ", f=0; while(y){f^=y&" << ((1u << lb) - 1) << "u; y>>=" << lb
+              << ";} tl^=f;}\n";
+        }
+        if (si == 0) {
+            for (int s = 0; s < R; ++s) o << reg(s) << "=psi[g+" << goff[s] << "ull];";
+            o << "\n";
+        } else {
+            o << "__syncthreads();\n";
+            for (int s = 0; s < R; ++s) o << reg(s) << "=sm[tl^" << loff[s] << "u];";
+            o << "\n";
+        }
+        for (const LOp& op : st.ops) emit_op(e, op, sc, fac);
+        if (si + 1 == sym.stages.size()) {
+            if (!is1(fac)) {
+                o << "// deferred scalar factor of the pass\n";
+                for (int s = 0; s < R; ++s) {
+                    auto mm = mul(e, reg(s), fac);
+                    o << reg(s) << "=mk(" << mm.first << "," << mm.second << ");";
+                }
+                o << "\n";
+            }
+            for (int s = 0; s < R; ++s) o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
+            o << "\n";
+        } else {
+            for (int s = 0; s < R; ++s) o << "sm[tl^" << loff[s] << "u]=" << reg(s) << ";";
+            o << "\n";
+        }
+    }
+    o << "}\n";
+    return o.str();
+}
+
+// ------------------------------------------------------------------ compile + cache
+namespace {
+std::mutex g_mu;
+std::unordered_map<std::string, void*> g_cache;  // key: device + source
+
+std::string nvrtc_log(nvrtcProgram p) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(p, &n);
+    std::string s(n, '\0');
+    if (n) nvrtcGetProgramLog(p, &s[0]);
+    return s;
+}
+}  // namespace
+
+sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::string& err) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::string key = std::to_string(dev) + "\n" + src;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_cache.find(key);
+        if (it != g_cache.end()) {
+            *fn_out = it->second;
+            return SV_OK;
+        }
+    }
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), "svpass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+        err = "nvrtcCreateProgram failed";
+        return SV_ERR_CUDA;
+    }
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=true"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+    if (rc != NVRTC_SUCCESS) {
+        err = std::string("nvrtc: ") + nvrtcGetErrorString(rc) + "\n" + nvrtc_log(prog).substr(0, 4000);
+        nvrtcDestroyProgram(&prog);
+        return SV_ERR_CUDA;
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    std::string cubin(n, '\0');
+    nvrtcGetCUBIN(prog, &cubin[0]);
+    nvrtcDestroyProgram(&prog);
+    // runtime library API (no direct libcuda link): load the cubin, fetch the kernel handle
+    cudaLibrary_t lib;
+    cudaError_t ce = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (ce != cudaSuccess) {
+        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(ce);
+        return SV_ERR_CUDA;
+    }
+    cudaKernel_t fn;
+    ce = cudaLibraryGetKernel(&fn, lib, "svpass");
+    if (ce == cudaSuccess && smem > 48 * 1024)
+        ce = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ce != cudaSuccess) {
+        err = std::string("cudaLibraryGetKernel/cudaFuncSetAttribute: ") + cudaGetErrorString(ce);
+        return SV_ERR_CUDA;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_cache.emplace(key, (void*)fn);
+    *fn_out = (void*)fn;
+    return SV_OK;
+}
+
+sv_status jit_prepare(Schedule& sc, std::string& err) {
+    std::vector<PassPlan*> todo;
+    for (PassPlan& pp : sc.passes)
+        if (pp.kind == PassPlan::TILE && pp.sym && !pp.jit_fn) todo.push_back(&pp);
+    if (todo.empty()) return SV_OK;
+    std::vector<std::string> srcs(todo.size());
+    for (size_t i = 0; i < todo.size(); ++i)
+        srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->jit_threads, todo[i]->jit_smem);
+    std::vector<sv_status> st(todo.size(), SV_OK);
+    std::vector<std::string> errs(todo.size());
+    std::vector<void*> fns(todo.size(), nullptr);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t nthr = std::max<size_t>(1, std::min<size_t>(todo.size(), std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < nthr; ++w)
+        pool.emplace_back([&, w]() {
+            cudaSetDevice(dev);
+            for (size_t i = w; i < todo.size(); i += nthr)
+                st[i] = jit_compile(srcs[i], todo[i]->jit_smem, &fns[i], errs[i]);
+        });
+    for (auto& th : pool) th.join();
+    for (size_t i = 0; i < todo.size(); ++i) {
+        if (st[i] != SV_OK) {
+            err = errs[i];
+            return st[i];
+        }
+        todo[i]->jit_fn = fns[i];
+    }
+    return SV_OK;
+}
+
+cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream) {
+    void* args[] = {&psi};
+    return cudaLaunchKernel(pp.jit_fn, dim3((unsigned)pp.ntiles), dim3((unsigned)pp.jit_threads), args,
+                            pp.jit_smem, stream);
+}
+
+}  // namespace svb

@@ -1,0 +1,17 @@
+// jit.hpp -- per-pass specialised kernels (generated CUDA, NVRTC for sm_100a).
+#pragma once
+#include <string>
+
+#include "engine.hpp"
+
+namespace svb {
+
+// CUDA source of one fused tile pass; returns the launch shape.
+std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem);
+// Compile (or fetch from the in-process cache) and return a CUfunction.
+sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::string& err);
+// Compile every TILE pass of a schedule that has no kernel yet (parallel over passes).
+sv_status jit_prepare(Schedule& sc, std::string& err);
+cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream);
+
+}  // namespace svb

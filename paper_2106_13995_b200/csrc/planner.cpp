@@ -259,21 +259,45 @@ std::vector<cd> swap_bits_u2(const std::vector<cd>& M) {
     return R;
 }
 
+// Symbolic pass: tile qubits, and per stage the register order (wide-op targets first, then
+// the other needed qubits, then padding with the highest free tile qubits so the low qubits
+// stay lane bits for coalescing).
+bool make_sym(const std::vector<const LOp*>& ops, const std::vector<StagePlan>& stages, uint64_t S, int rb,
+              bool dbl, TileSym& sym, std::string& err) {
+    sym.tq.clear();
+    for (int q = 0; q < 64; ++q)
+        if ((S >> q) & 1) sym.tq.push_back(q);
+    const int m = (int)sym.tq.size();
+    if (m > kMaxTileQubits || m < rb) { err = "internal: bad tile size"; return false; }
+    sym.rb = rb;
+    sym.dbl = dbl;
+    sym.stages.clear();
+    for (const StagePlan& sp : stages) {
+        StageSym ss;
+        ss.rq = sp.wide;
+        for (int q = 0; q < 64; ++q)
+            if (((sp.R >> q) & 1) && std::find(ss.rq.begin(), ss.rq.end(), q) == ss.rq.end()) ss.rq.push_back(q);
+        for (int b = m - 1; b >= 0 && (int)ss.rq.size() < rb; --b)
+            if (std::find(ss.rq.begin(), ss.rq.end(), sym.tq[b]) == ss.rq.end()) ss.rq.push_back(sym.tq[b]);
+        if ((int)ss.rq.size() != rb) { err = "internal: register set size"; return false; }
+        for (int oi : sp.ops) ss.ops.push_back(*ops[oi]);
+        sym.stages.push_back(std::move(ss));
+    }
+    return true;
+}
+
 template <typename real>
-bool write_tile_params(const std::vector<const LOp*>& ops, const std::vector<StagePlan>& stages, uint64_t S,
-                       int rb, const Context& ctx, PassPlan& pp, std::string& err) {
+bool write_tile_params(const TileSym& sym, const Context& ctx, PassPlan& pp, std::string& err) {
     pp.kind = PassPlan::TILE;
     pp.params.assign(sizeof(PassParams<real>), 0);
     auto* P = reinterpret_cast<PassParams<real>*>(pp.params.data());
     PassHeader& h = P->h;
-    std::vector<int> tq;
-    for (int q = 0; q < 64; ++q)
-        if ((S >> q) & 1) tq.push_back(q);
+    const std::vector<int>& tq = sym.tq;
+    const int rb = sym.rb;
     const int m = (int)tq.size();
-    if (m > kMaxTileQubits || m < rb) { err = "internal: bad tile size"; return false; }
     h.m = (uint8_t)m;
     h.rb = (uint8_t)rb;
-    h.nstages = (uint8_t)stages.size();
+    h.nstages = (uint8_t)sym.stages.size();
     h.n_local = (uint32_t)ctx.nl;
     int local_of[64];
     for (int i = 0; i < 64; ++i) local_of[i] = -1;
@@ -281,16 +305,10 @@ bool write_tile_params(const std::vector<const LOp*>& ops, const std::vector<Sta
     const int lb = sizeof(real) == 4 ? 4 : 3;
     const int R = 1 << rb;
     int nop = 0, ncoef = 0;
+    const auto& stages = sym.stages;
     for (size_t si = 0; si < stages.size(); ++si) {
-        const StagePlan& sp = stages[si];
         StageDesc& sd = h.stage[si];
-        // register order: wide-op targets first, then other needed qubits, then padding
-        std::vector<int> rq = sp.wide;
-        for (int q = 0; q < 64; ++q)
-            if (((sp.R >> q) & 1) && std::find(rq.begin(), rq.end(), q) == rq.end()) rq.push_back(q);
-        for (int b = m - 1; b >= 0 && (int)rq.size() < rb; --b)
-            if (std::find(rq.begin(), rq.end(), tq[b]) == rq.end()) rq.push_back(tq[b]);
-        if ((int)rq.size() != rb) { err = "internal: register set size"; return false; }
+        const std::vector<int>& rq = stages[si].rq;
         int regpos_of[64];
         for (int i = 0; i < 64; ++i) regpos_of[i] = -1;
         for (int j = 0; j < rb; ++j) { sd.rpos[j] = (uint8_t)local_of[rq[j]]; regpos_of[rq[j]] = j; }
@@ -307,8 +325,7 @@ bool write_tile_params(const std::vector<const LOp*>& ops, const std::vector<Sta
             if (si + 1 == stages.size()) h.goff_last[s] = go;
         }
         sd.op_begin = (uint16_t)nop;
-        for (int oi : sp.ops) {
-            const LOp& lo = *ops[oi];
+        for (const LOp& lo : stages[si].ops) {
             if (nop >= kMaxOps) { err = "internal: op overflow"; return false; }
             OpDesc& od = h.op[nop++];
             od.kind = (uint8_t)lo.kind;
@@ -370,7 +387,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
     const int m_pad = std::min(rb + 8, nl);       // single-stage passes: 256 threads
     const int L = std::min(dbl ? 4 : 5, nl);      // low qubits: contiguous 256-byte runs
     const uint64_t lowmask = (L >= 64) ? ~0ull : ((1ull << L) - 1);
-    const bool per_gate = !o.fuse || o.force_kernel != SV_KERNEL_AUTO;
+    const bool per_gate = !o.fuse || o.force_kernel == SV_KERNEL_PER_GATE || o.force_kernel == SV_KERNEL_DENSE;
 
     std::vector<int> remaining(ops.size());
     for (size_t i = 0; i < ops.size(); ++i) {
@@ -464,8 +481,10 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
         std::vector<const LOp*> pops;  // stage op indices refer to this list
         for (int idx : pass_ops) pops.push_back(&ops[idx]);
         PassPlan pp;
-        const bool ok = dbl ? write_tile_params<double>(pops, stages, S, rb, ctx, pp, err)
-                            : write_tile_params<float>(pops, stages, S, rb, ctx, pp, err);
+        pp.sym = std::make_shared<TileSym>();
+        if (!make_sym(pops, stages, S, rb, dbl, *pp.sym, err)) return SV_ERR_STATE;
+        const bool ok = dbl ? write_tile_params<double>(*pp.sym, ctx, pp, err)
+                            : write_tile_params<float>(*pp.sym, ctx, pp, err);
         if (!ok) return SV_ERR_STATE;
         out.stages += stages.size();
         out.passes.push_back(std::move(pp));

@@ -14,6 +14,7 @@
 #include <cstring>
 
 #include "comm.hpp"
+#include "jit.hpp"
 
 using namespace svb;
 
@@ -55,9 +56,14 @@ sv_status run_ops(sv_state_s* s, std::vector<std::vector<LOp>>& ops, const RunOp
         const Context ctx = make_ctx(s, rank_of(s, i));
         sv_status r = build_schedule(ops[i], ctx, o, sc, err);
         if (r != SV_OK) return r;
+        if (o.use_jit()) {
+            r = jit_prepare(sc, err);
+            if (r != SV_OK) return r;
+        }
         void* psi = s->shard_ptr(i);
         for (const PassPlan& pp : sc.passes) {
-            cudaError_t e = pp.kind == PassPlan::TILE
+            cudaError_t e = (pp.kind == PassPlan::TILE && pp.jit_fn) ? jit_launch(pp, psi, s->stream)
+                            : pp.kind == PassPlan::TILE
                                 ? launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles,
                                                    s->stream)
                                 : launch_dense_k(s->dbl, psi, pp.params.data(), pp.groups, s->stream);

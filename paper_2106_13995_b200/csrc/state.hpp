@@ -43,6 +43,7 @@ struct sv_plan_s {
     svb::RunOpts opts;
     // schedule cache for the identity qubit map on one unsharded GPU
     bool cached = false;
+    bool jitted = false;
     svb::Schedule sched;
     uint64_t hbm_bytes = 0;
     cudaGraphExec_t graph = nullptr;

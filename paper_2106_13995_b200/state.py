@@ -55,6 +55,14 @@ class Plan:
         check(lib.sv_plan_info(self._h, ctypes.byref(n), ctypes.byref(g), ctypes.byref(p), ctypes.byref(s)))
         return {"n": n.value, "gates": g.value, "passes": p.value, "stages": s.value}
 
+    def source(self, i: int) -> str:
+        """Generated CUDA source of tile pass i (single-GPU schedule)."""
+        ln = ctypes.c_size_t()
+        check(lib.sv_plan_source(self._h, int(i), None, 0, ctypes.byref(ln)))
+        buf = ctypes.create_string_buffer(ln.value + 1)
+        check(lib.sv_plan_source(self._h, int(i), buf, ln.value + 1, ctypes.byref(ln)))
+        return buf.value.decode()
+
     def close(self):
         if self._h:
             lib.sv_plan_destroy(self._h)

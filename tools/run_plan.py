@@ -1,0 +1,31 @@
+"""Profiling driver: run one circuit plan `reps` times on a fresh state (for ncu captures).
+
+python tools/run_plan.py [--workload supremacy|multiplier] [--dtype c64] [--qubits 30] [--reps 2]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import workloads as W  # noqa: E402
+import paper_2106_13995_b200 as P  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="supremacy")
+ap.add_argument("--dtype", default="c64")
+ap.add_argument("--qubits", type=int, default=30)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--fuse", type=int, default=1)
+a = ap.parse_args()
+if a.workload == "supremacy":
+    c = W.supremacy(6, 5, 20, 0) if a.qubits == 30 else W.supremacy((a.qubits + 4) // 5, 5, 20, 0, n=a.qubits)
+else:
+    c = W.multiplier(8, 7)
+plan = P.Plan(W.to_text(c), a.dtype, fuse=bool(a.fuse))
+with P.StateVector(c.n, a.dtype) as sv:
+    for _ in range(a.reps):
+        sv.init_zero()
+        st = sv.apply_plan(plan)
+    sv.sync()
+print(st, plan.info())

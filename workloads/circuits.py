@@ -102,11 +102,13 @@ class Xoshiro256ss:
 
 
 # ---------------------------------------------------------------- supremacy (App. C)
-def _cz_pattern(rows: int, cols: int, t: int) -> List[Tuple[int, int]]:
+def _cz_pattern(rows: int, cols: int, t: int, n: Optional[int] = None) -> List[Tuple[int, int]]:
     """CZ layer pat[t mod 8]: H(0,0), H(1,1), V(0,0), V(1,1), H(0,1), H(1,0), V(0,1), V(1,0).
 
     H(s,u) = {(r,c)-(r,c+1) : c = s, r = u (mod 2)};  V(s,u) = {(r,c)-(r+1,c) : r = s, c = u (mod 2)}.
+    With n < rows*cols only the first n sites (row-major) exist (partial last row).
     """
+    n = rows * cols if n is None else n
     pats = [("H", 0, 0), ("H", 1, 1), ("V", 0, 0), ("V", 1, 1),
             ("H", 0, 1), ("H", 1, 0), ("V", 0, 1), ("V", 1, 0)]
     kind, s, u = pats[t % 8]
@@ -114,26 +116,29 @@ def _cz_pattern(rows: int, cols: int, t: int) -> List[Tuple[int, int]]:
     for r in range(rows):
         for c in range(cols):
             q = r * cols + c
-            if kind == "H" and c % 2 == s and r % 2 == u and c + 1 < cols:
+            if kind == "H" and c % 2 == s and r % 2 == u and c + 1 < cols and q + 1 < n:
                 pairs.append((q, q + 1))
-            if kind == "V" and r % 2 == s and c % 2 == u and r + 1 < rows:
+            if kind == "V" and r % 2 == s and c % 2 == u and r + 1 < rows and q + cols < n:
                 pairs.append((q, q + cols))
     return pairs
 
 
-def supremacy(rows: int, cols: int, depth: int, seed: int = 0) -> Circuit:
+def supremacy(rows: int, cols: int, depth: int, seed: int = 0, n: Optional[int] = None) -> Circuit:
     """Supremacy-style grid circuit (reading R6).
 
     Moment 0: H on every qubit.  Cycle t: CZ layer pat[t mod 8], then a single-qubit
     layer on every qubit not in that CZ layer: first gate T, afterwards uniform over
     {SqrtX, SqrtY, T} minus the qubit's previous gate.  `depth` counts cycles.
+    n (default rows*cols) keeps only the first n sites of the grid (partial last row), used
+    for the 2^30-amplitudes-per-GPU weak-scaling widths 31..33.
     """
-    n = rows * cols
+    n = rows * cols if n is None else n
+    assert 2 <= n <= rows * cols
     rng = Xoshiro256ss(seed)
     moments: List[List[GateSpec]] = [[GateSpec("H", (q,)) for q in range(n)]]
     prev: List[Optional[str]] = [None] * n
     for t in range(depth):
-        pairs = _cz_pattern(rows, cols, t)
+        pairs = _cz_pattern(rows, cols, t, n)
         moments.append([GateSpec("CZ", p) for p in pairs])
         busy = {q for p in pairs for q in p}
         layer = []
