@@ -76,6 +76,7 @@ typedef struct {
     int force_kernel;    /* sv_kernel */
     int check_unitary;   /* 1 = reject matrices with |U^dagger U - I| > 1e-9 */
     int use_graph;       /* 1 = record the plan's launches into a CUDA graph on first use */
+    int profile;         /* 1 = bracket every pass with CUDA events (sv_plan_pass_times) */
 } sv_run_opts;
 
 typedef struct {
@@ -148,6 +149,11 @@ sv_status sv_plan_destroy(sv_plan p);
 
 /* Apply a compiled plan to a state (asynchronous).  stats may be NULL. */
 sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats);
+
+/* Device time of every pass of the last sv_plan_apply of a plan compiled with
+ * opts.profile = 1 (CUDA events on the state's stream; synchronises).  Writes up to cap
+ * values (ms) and the pass count to *n. */
+sv_status sv_plan_pass_times(sv_plan p, float* ms_out, int cap, int* n);
 
 /* Parse + plan + apply every gate of every moment in order.  opts and stats
  * may be NULL; stats->gates equals the IR gate count. */

@@ -24,7 +24,8 @@ class SvError(RuntimeError):
 
 class RunOpts(ctypes.Structure):
     _fields_ = [("fuse", ctypes.c_int), ("tile_qubits", ctypes.c_int), ("max_fused_k", ctypes.c_int),
-                ("force_kernel", ctypes.c_int), ("check_unitary", ctypes.c_int), ("use_graph", ctypes.c_int)]
+                ("force_kernel", ctypes.c_int), ("check_unitary", ctypes.c_int), ("use_graph", ctypes.c_int),
+                ("profile", ctypes.c_int)]
 
 
 class RunStats(ctypes.Structure):
@@ -40,7 +41,7 @@ def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2106_13995_b200.build` "
                           "(there is no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    L = ctypes.CDLL(LIB_PATH)
     vp, cp, i, u64 = ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_uint64
     ip = ctypes.POINTER(ctypes.c_int)
     dp = ctypes.POINTER(ctypes.c_double)
@@ -62,6 +63,7 @@ def _load():
         "sv_plan_destroy": (i, [vp]),
         "sv_plan_source": (i, [vp, i, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "sv_plan_apply": (i, [vp, vp, ctypes.POINTER(RunStats)]),
+        "sv_plan_pass_times": (i, [vp, ctypes.POINTER(ctypes.c_float), i, ip]),
         "sv_apply_circuit": (i, [vp, cp, ctypes.POINTER(RunOpts), ctypes.POINTER(RunStats)]),
         "sv_amplitudes": (i, [vp, u64, u64, vp]),
         "sv_probabilities": (i, [vp, ip, i, dp]),
@@ -85,7 +87,7 @@ lib = _load()
 EXPORTED = ["sv_memory_estimate", "sv_create", "sv_wrap", "sv_nccl_unique_id", "sv_create_sharded",
             "sv_create_virtual_sharded", "sv_destroy", "sv_init_zero", "sv_init_basis", "sv_init_uniform",
             "sv_set_amplitudes", "sv_apply_gate", "sv_plan_compile", "sv_plan_info", "sv_plan_source",
-            "sv_plan_destroy",
+            "sv_plan_destroy", "sv_plan_pass_times",
             "sv_plan_apply", "sv_apply_circuit", "sv_amplitudes", "sv_probabilities", "sv_norm", "sv_sync",
             "sv_info", "sv_device_ptr", "sv_stream", "sv_qubit_map", "sv_last_error", "sv_version"]
 

@@ -57,6 +57,7 @@ RunOpts to_opts(const sv_run_opts* o) {
         r.force_kernel = o->force_kernel;
         r.check_unitary = o->check_unitary != 0;
         r.use_graph = o->use_graph != 0;
+        r.profile = o->profile != 0;
     }
     return r;
 }
@@ -126,8 +127,19 @@ double uniform_amp(int n) {
 int shard_count(const sv_state_s* s) { return s->virt ? s->world : 1; }
 int shard_rank(const sv_state_s* s, int i) { return s->virt ? i : s->rank; }
 
-sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stats* st) {
+sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stats* st,
+                       std::vector<cudaEvent_t>* ev = nullptr) {
+    if (ev) {
+        while (ev->size() < sc.passes.size() + 1) {
+            cudaEvent_t x;
+            CK(cudaEventCreate(&x));
+            ev->push_back(x);
+        }
+        CK(cudaEventRecord((*ev)[0], s->stream));
+    }
+    size_t pi = 0;
     for (const PassPlan& pp : sc.passes) {
+        ++pi;
         cudaError_t e;
         if (pp.kind == PassPlan::TILE && pp.jit_fn)
             e = jit_launch(pp, psi, s->stream);
@@ -136,6 +148,7 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
         else
             e = launch_dense_k(s->dbl, psi, pp.params.data(), pp.groups, s->stream);
         if (e != cudaSuccess) return cuda_fail(e, "pass launch");
+        if (ev) CK(cudaEventRecord((*ev)[pi], s->stream));
         if (st) {
             st->passes += 1;
             st->launches += 1;
@@ -442,7 +455,19 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     return SV_OK;
 }
 
+sv_status sv_plan_pass_times(sv_plan p, float* ms_out, int cap, int* n) {
+    if (!p) return fail(SV_ERR_ARG, "NULL plan");
+    if (n) *n = p->prof_n;
+    for (int i = 0; i < p->prof_n && i < cap && ms_out; ++i) {
+        CK(cudaEventSynchronize(p->prof_ev[i + 1]));
+        CK(cudaEventElapsedTime(&ms_out[i], p->prof_ev[i], p->prof_ev[i + 1]));
+    }
+    return SV_OK;
+}
+
 sv_status sv_plan_destroy(sv_plan p) {
+    if (p)
+        for (cudaEvent_t x : p->prof_ev) cudaEventDestroy(x);
     if (p && p->graph) cudaGraphExecDestroy(p->graph);
     delete p;
     return SV_OK;
@@ -501,7 +526,8 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
             stats->hbm_bytes = 2ull * s->local_amps() * s->amp_bytes() * tmp.passes;
         }
     } else {
-        st = run_schedule(s, s->d, p->sched, stats);
+        st = run_schedule(s, s->d, p->sched, stats, p->opts.profile ? &p->prof_ev : nullptr);
+        p->prof_n = p->opts.profile ? (int)p->sched.passes.size() : 0;
     }
     if (stats) stats->gates = p->circ.gates.size();
     return st;

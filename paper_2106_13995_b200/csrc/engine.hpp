@@ -63,6 +63,7 @@ struct RunOpts {
     int force_kernel = SV_KERNEL_AUTO;
     bool check_unitary = false;
     bool use_graph = false;
+    bool profile = false;
     bool use_jit() const { return fuse && force_kernel == SV_KERNEL_AUTO; }
 };
 

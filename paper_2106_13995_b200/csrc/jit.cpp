@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -63,6 +64,8 @@ std::pair<std::string, std::string> mul(const Em& e, const std::string& v, const
         if (ci == -1.0) return {y, "(-" + x + ")"};
         return {"(-" + y + ")*" + e.lit(ci), x + "*" + e.lit(ci)};
     }
+    if (cr == 1.0 && ci == 1.0) return {"(" + x + "-" + y + ")", "(" + x + "+" + y + ")"};
+    if (cr == 1.0 && ci == -1.0) return {"(" + x + "+" + y + ")", "(" + y + "-" + x + ")"};
     if (cr == ci) return {"(" + x + "-" + y + ")*" + e.lit(cr), "(" + x + "+" + y + ")*" + e.lit(cr)};
     if (cr == -ci) return {"(" + x + "+" + y + ")*" + e.lit(cr), "(" + y + "-" + x + ")*" + e.lit(cr)};
     return {x + "*" + e.lit(cr) + "-" + y + "*" + e.lit(ci), x + "*" + e.lit(ci) + "+" + y + "*" + e.lit(cr)};
@@ -70,12 +73,67 @@ std::pair<std::string, std::string> mul(const Em& e, const std::string& v, const
 
 std::string reg(int s) { return "v[" + std::to_string(s) + "]"; }
 
+// ---- packed backend (complex64): one amplitude = one 64-bit register pair (re, im) driven by
+// the sm_100 paired FP32 instructions (FADD2 / FMUL2 / FFMA2).  ptxas folds the swaps and
+// partial negations of i*v and -i*v into operand modifiers (.LO_HI / .NP), so multiplying by
+// +-1 or +-i is free and a complex butterfly is 2 instructions per amplitude pair.
+std::string k2(double a, double b) {
+    const float fa = (float)a, fb = (float)b;
+    uint32_t ua, ub;
+    memcpy(&ua, &fa, 4);
+    memcpy(&ub, &fb, 4);
+    char buf[40];
+    snprintf(buf, sizeof buf, "0x%016llxull", (unsigned long long)ua | ((unsigned long long)ub << 32));
+    return buf;
+}
+
+// acc + c * v  (acc empty: c * v)
+std::string f2_term(const std::string& acc, const std::string& v, const cd& c) {
+    const double cr = c.real(), ci = c.imag();
+    std::string u;
+    if (ci == 0.0 && cr == 1.0) u = v;
+    else if (ci == 0.0 && cr == -1.0) u = "N(" + v + ")";
+    else if (cr == 0.0 && ci == 1.0) u = "I(" + v + ")";
+    else if (cr == 0.0 && ci == -1.0) u = "NI(" + v + ")";
+    if (!u.empty()) return acc.empty() ? u : "A(" + acc + "," + u + ")";
+    if (std::abs(cr) == 1.0 && std::abs(ci) == 1.0) {
+        // (+-1 +- i) v = +-v +- i v: one FADD2 with operand modifiers
+        const std::string a = cr > 0 ? v : "N(" + v + ")";
+        const std::string b = ci > 0 ? "I(" + v + ")" : "NI(" + v + ")";
+        const std::string t = "A(" + a + "," + b + ")";
+        return acc.empty() ? t : "A(" + acc + "," + t + ")";
+    }
+    if (ci == 0.0) return acc.empty() ? "M(" + v + "," + k2(cr, cr) + ")" : "F(" + v + "," + k2(cr, cr) + "," + acc + ")";
+    if (cr == 0.0) return acc.empty() ? "M(I(" + v + ")," + k2(ci, ci) + ")"
+                                      : "F(I(" + v + ")," + k2(ci, ci) + "," + acc + ")";
+    const std::string inner =
+        acc.empty() ? "M(" + v + "," + k2(cr, cr) + ")" : "F(" + v + "," + k2(cr, cr) + "," + acc + ")";
+    return "F(I(" + v + ")," + k2(ci, ci) + "," + inner + ")";
+}
+
+// expression (of type C) for c * v
+std::string scaled(const Em& e, const std::string& v, const cd& c) {
+    if (!e.dbl) return f2_term("", v, c);
+    auto p = mul(e, v, c);
+    return "mk(" + p.first + "," + p.second + ")";
+}
+
 // out_r = sum_c M[r][c] in_c for a d x d matrix over registers idx[0..d-1]
 void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M) {
     const size_t d = idx.size();
     e.o << "{";
     for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
     for (size_t r = 0; r < d; ++r) {
+        if (!e.dbl) {
+            std::string acc;
+            for (size_t c = 0; c < d; ++c) {
+                const cd m = M[r * d + c];
+                if (is0(m)) continue;
+                acc = f2_term(acc, "i" + std::to_string(c), m);
+            }
+            e.o << reg(idx[r]) << "=" << (acc.empty() ? std::string("0ull") : acc) << ";";
+            continue;
+        }
         std::string re, im;
         for (size_t c = 0; c < d; ++c) {
             const cd m = M[r * d + c];
@@ -123,8 +181,70 @@ struct StageCtx {
     int pos[64];  // physical qubit -> register position, -1 if not a register bit
 };
 
-void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
+// Pending per-qubit diagonal factors diag(s0, s1) not yet multiplied into the registers
+// (the 1/sqrt2 of T and Tdg).  They commute with every op except a non-diagonal op that
+// targets the qubit, which absorbs them into its matrix columns (its butterfly adds become
+// FFMAs at no extra cost), or the end of the pass, where they join the deferred factor.
+using Pend = std::map<int, std::pair<cd, cd>>;
+
+// Deferred state of a pass while its code is generated:
+//   fac  -- scalar factor (butterfly normalisations), applied once at the end of the pass;
+//   pend -- per-qubit diagonal factors (above);
+//   ph   -- per-register unit phase (+-1, +-i) from Z, S, CZ, ...: never multiplied on its
+//           own, it is folded into the next op that reads the register (a column of its
+//           matrix, or an operand modifier of the packed FP32 instruction), so those diagonal
+//           gates cost no instruction at all.
+struct PassState {
+    cd fac = 1;
+    Pend pend;
+    std::vector<cd> ph;
+};
+
+bool is_unit(const cd& c) {
+    return c == cd(1, 0) || c == cd(-1, 0) || c == cd(0, 1) || c == cd(0, -1);
+}
+
+// multiply register s by its pending unit phase now
+void flush_ph(Em& e, PassState& ps, int s) {
+    if (is1(ps.ph[s])) return;
+    e.o << reg(s) << "=" << scaled(e, reg(s), ps.ph[s]) << ";";
+    ps.ph[s] = 1;
+}
+
+// multiply the registers by a pending per-qubit factor now (controlled ops on the qubit need it)
+void emit_flush(Em& e, const StageCtx& sc, PassState& ps, int q) {
+    auto it = ps.pend.find(q);
+    if (it == ps.pend.end()) return;
+    const cd s0 = it->second.first, s1 = it->second.second;
+    ps.pend.erase(it);
     const int R = 1 << sc.rb;
+    const int pq = sc.pos[q];
+    if (pq >= 0) {
+        for (int s = 0; s < R; ++s) {
+            const cd c = (((s >> pq) & 1) ? s1 : s0) * ps.ph[s];
+            ps.ph[s] = 1;
+            if (is1(c)) continue;
+            e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
+        }
+        e.o << "\n";
+    } else {
+        for (int s = 0; s < R; ++s) flush_ph(e, ps, s);
+        e.o << "{const bool b=((g>>" << q << ")&1ull)!=0;";
+        for (int br = 0; br < 2; ++br) {
+            const cd c = br ? s1 : s0;
+            if (is1(c)) continue;
+            e.o << (br ? "if(b){" : "if(!b){");
+            for (int s = 0; s < R; ++s) e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
+            e.o << "}";
+        }
+        e.o << "}\n";
+    }
+}
+
+void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
+    const int R = 1 << sc.rb;
+    cd& fac = ps.fac;
+    Pend& pend = ps.pend;
     uint32_t creg = 0;
     uint64_t cm = 0;
     for (int c : op.ctrl) {
@@ -132,11 +252,55 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
         else cm |= 1ull << c;
     }
     const bool controlled = !op.ctrl.empty();
-    if (cm) e.o << "if((g&" << cm << "ull)==" << cm << "ull){\n";
-    auto sel = [&](int s) { return (s & creg) == creg; };
     const int k = (int)op.tq.size();
+    auto sel = [&](int s) { return (s & creg) == creg; };
     std::vector<int> p(k);
     for (int j = 0; j < k; ++j) p[j] = sc.pos[op.tq[j]];
+    uint32_t tmask = 0;
+    for (int j = 0; j < k; ++j) tmask |= 1u << p[j];
+    // registers the op may write
+    std::vector<int> touched;
+    for (int s = 0; s < R; ++s)
+        if (sel(s)) touched.push_back(s);
+    // Branch-free sign flips: a diagonal op with factor -1 (Z, CZ, CCZ, ...) whose condition
+    // involves non-register bits becomes one FMUL2 by a per-thread sign per affected register.
+    if (!e.dbl && k == 0 && (op.kind == OP_Z || (op.kind == OP_PHASE && op.coef[0] == cd(-1, 0))) &&
+        op.dq.size() == 1) {
+        const int q = op.dq[0], pq = sc.pos[q];
+        if (cm || pq < 0) {
+            std::string cond = cm ? "((g&" + std::to_string(cm) + "ull)==" + std::to_string(cm) + "ull)" : "true";
+            if (pq < 0) cond += "&&((g>>" + std::to_string(q) + ")&1ull)";
+            e.o << "{const C sg=(" << cond << ")?" << k2(-1, -1) << ":" << k2(1, 1) << ";";
+            for (int s : touched) {
+                if (pq >= 0 && !((s >> pq) & 1)) continue;
+                e.o << reg(s) << "=M(" << scaled(e, reg(s), ps.ph[s]) << ",sg);";
+                ps.ph[s] = 1;
+            }
+            e.o << "}\n";
+            return;
+        }
+    }
+    // pending factors on the targets of a non-diagonal op
+    if (k > 0) {
+        if (controlled) {
+            for (int q : op.tq) emit_flush(e, sc, ps, q);
+        } else if (op.kind == OP_X || op.kind == OP_Y) {
+            auto it = pend.find(op.tq[0]);
+            if (it != pend.end()) std::swap(it->second.first, it->second.second);  // X D = D' X
+        } else if (op.kind == OP_SWAP) {
+            auto a = pend.find(op.tq[0]), b = pend.find(op.tq[1]);
+            std::pair<cd, cd> pa = a != pend.end() ? a->second : std::make_pair(cd(1), cd(1));
+            std::pair<cd, cd> pb = b != pend.end() ? b->second : std::make_pair(cd(1), cd(1));
+            pend.erase(op.tq[0]);
+            pend.erase(op.tq[1]);
+            if (!(is1(pb.first) && is1(pb.second))) pend[op.tq[0]] = pb;
+            if (!(is1(pa.first) && is1(pa.second))) pend[op.tq[1]] = pa;
+        }
+    }
+    // a run-time guard (control on a non-register bit) must see a consistent phase state
+    if (cm)
+        for (int s : touched) flush_ph(e, ps, s);
+    if (cm) e.o << "if((g&" << cm << "ull)==" << cm << "ull){\n";
     switch (op.kind) {
         case OP_U1: case OP_H: case OP_SX: case OP_SXDG: case OP_SY: case OP_SYDG: case OP_X: case OP_Y:
         case OP_U2: case OP_U3: case OP_U4: case OP_SWAP: {
@@ -154,8 +318,17 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
                 }
             }
             fac *= f;
-            uint32_t tmask = 0;
-            for (int j = 0; j < k; ++j) tmask |= 1u << p[j];
+            if (!controlled && op.kind != OP_X && op.kind != OP_Y && op.kind != OP_SWAP) {
+                // absorb pending factors of the targets into the matrix columns
+                const int d = 1 << k;
+                for (int j = 0; j < k; ++j) {
+                    auto it = pend.find(op.tq[j]);
+                    if (it == pend.end()) continue;
+                    for (int r = 0; r < d; ++r)
+                        for (int c = 0; c < d; ++c) M[r * d + c] *= ((c >> j) & 1) ? it->second.second : it->second.first;
+                    pend.erase(it);
+                }
+            }
             const int d = 1 << k;
             for (int s = 0; s < R; ++s) {
                 if (s & tmask) continue;
@@ -168,15 +341,26 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
                     idx[c] = x;
                 }
                 if (op.kind == OP_SWAP || op.kind == OP_X) {
-                    // pure register permutation: M[r][c] == 1 at one c per row
+                    // pure register permutation (M[r][c] == 1 at one c per row): the pending
+                    // phases travel with the values, no instruction at all
                     e.o << "{";
                     for (int c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+                    std::vector<cd> nph(d);
                     for (int r = 0; r < d; ++r)
                         for (int c = 0; c < d; ++c)
-                            if (is1(M[r * d + c])) e.o << reg(idx[r]) << "=i" << c << ";";
+                            if (is1(M[r * d + c])) {
+                                e.o << reg(idx[r]) << "=i" << c << ";";
+                                nph[r] = ps.ph[idx[c]];
+                            }
+                    for (int r = 0; r < d; ++r) ps.ph[idx[r]] = nph[r];
                     e.o << "}\n";
                 } else {
-                    emit_dense(e, idx, M);
+                    // fold the inputs' pending phases into the matrix columns
+                    std::vector<cd> Mp = M;
+                    for (int c = 0; c < d; ++c)
+                        for (int r = 0; r < d; ++r) Mp[r * d + c] *= ps.ph[idx[c]];
+                    for (int c = 0; c < d; ++c) ps.ph[idx[c]] = 1;
+                    emit_dense(e, idx, Mp);
                 }
             }
         } break;
@@ -189,28 +373,51 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
             else c1 = diag_const(op.kind);
             const int q = op.dq.empty() ? -1 : op.dq[0];
             const int pq = q >= 0 ? sc.pos[q] : -1;
-            if (q >= 0 && pq < 0) {
+            if ((op.kind == OP_T || op.kind == OP_TDG) && !controlled && pq >= 0) {
+                // e^{+-i pi/4} = (1 +- i) / sqrt2: multiply by (1 +- i) now, defer the 1/sqrt2
+                c1 = op.kind == OP_T ? cd(1, 1) : cd(1, -1);
+                auto it = pend.find(q);
+                if (it == pend.end()) it = pend.emplace(q, std::make_pair(cd(1), cd(1))).first;
+                it->second.second *= 0.70710678118654752440;
+            }
+            if (op.kind == OP_SCALAR && !controlled) {
+                fac *= c0;  // a global phase/scale: join the deferred scalar
+                break;
+            }
+            const bool real_signs = c0.imag() == 0.0 && c1.imag() == 0.0 && std::abs(c0.real()) == 1.0 &&
+                                    std::abs(c1.real()) == 1.0;
+            if (q >= 0 && pq < 0 && !e.dbl && real_signs && !cm) {
+                // +-1 chosen by a non-register index bit: one branch-free FMUL2 per amplitude
+                // (the register's pending unit phase rides along as an operand modifier)
+                e.o << "{const C sg=((g>>" << q << ")&1ull)?" << k2(c1.real(), c1.real()) << ":"
+                    << k2(c0.real(), c0.real()) << ";";
+                for (int s : touched) {
+                    e.o << reg(s) << "=M(" << scaled(e, reg(s), ps.ph[s]) << ",sg);";
+                    ps.ph[s] = 1;
+                }
+                e.o << "}\n";
+            } else if (q >= 0 && pq < 0) {
                 // factor chosen by an index bit that is not a register bit
+                for (int s : touched) flush_ph(e, ps, s);
                 e.o << "{const bool b=((g>>" << q << ")&1ull)!=0;";
                 for (int br = 0; br < 2; ++br) {
                     const cd c = br ? c1 : c0;
                     if (is1(c)) continue;
                     e.o << (br ? "if(b){" : "if(!b){");
-                    for (int s = 0; s < R; ++s) {
-                        if (!sel(s)) continue;
-                        auto m = mul(e, reg(s), c);
-                        e.o << reg(s) << "=mk(" << m.first << "," << m.second << ");";
-                    }
+                    for (int s : touched) e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
                     e.o << "}";
                 }
                 e.o << "}\n";
             } else {
-                for (int s = 0; s < R; ++s) {
-                    if (!sel(s)) continue;
-                    const cd c = (pq < 0) ? c0 : (((s >> pq) & 1) ? c1 : c0);
+                for (int s : touched) {
+                    const cd c = ((pq < 0) ? c0 : (((s >> pq) & 1) ? c1 : c0)) * ps.ph[s];
+                    if (is_unit(c) && !cm) {
+                        ps.ph[s] = c;  // +-1, +-i: defer, folded into the next reader
+                        continue;
+                    }
+                    ps.ph[s] = 1;
                     if (is1(c)) continue;
-                    auto m = mul(e, reg(s), c);
-                    e.o << reg(s) << "=mk(" << m.first << "," << m.second << ");";
+                    e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
                 }
                 e.o << "\n";
             }
@@ -222,6 +429,7 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
             std::vector<int> rtq;
             if (p0 < 0) rtq.push_back(q0);
             if (p1 < 0) rtq.push_back(q1);
+            for (int s : touched) flush_ph(e, ps, s);
             e.o << "{";
             for (size_t j = 0; j < rtq.size(); ++j) e.o << "const int b" << j << "=(int)((g>>" << rtq[j] << ")&1ull);";
             for (int combo = 0; combo < (1 << rtq.size()); ++combo) {
@@ -237,8 +445,8 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, cd& fac) {
                     if (p1 >= 0) bi1 = (s >> p1) & 1; else bi1 = (combo >> ri++) & 1;
                     const cd c = op.coef[bi0 | (bi1 << 1)];
                     if (is1(c)) continue;
-                    auto m = mul(e, reg(s), c);
-                    e.o << reg(s) << "=mk(" << m.first << "," << m.second << ");";
+                    const std::string m = scaled(e, reg(s), c);
+                    e.o << reg(s) << "=" << m << ";";
                 }
                 if (!rtq.empty()) e.o << "}";
             }
@@ -290,9 +498,24 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
 
     auto& o = e.o;
     o << "// generated tile pass: m=" << m << " rb=" << rb << " stages=" << sym.stages.size() << "\n";
-    o << "typedef " << (sym.dbl ? "double" : "float") << " R;\n";
-    o << "struct alignas(" << (sym.dbl ? 16 : 8) << ") C { R x, y; };\n";
-    o << "__device__ __forceinline__ C mk(R x, R y){C c; c.x=x; c.y=y; return c;}\n";
+    if (sym.dbl) {
+        o << "typedef double R;\n";
+        o << "struct alignas(16) C { R x, y; };\n";
+        o << "__device__ __forceinline__ C mk(R x, R y){C c; c.x=x; c.y=y; return c;}\n";
+    } else {
+        // packed complex64: lo = re, hi = im; paired FP32 ops (sm_100)
+        o << "typedef unsigned long long C;\n"
+             "#define DI __device__ __forceinline__\n"
+             "DI C pk(float x,float y){C r;asm(\"mov.b64 %0,{%1,%2};\":\"=l\"(r):\"f\"(x),\"f\"(y));return r;}\n"
+             "DI float lo(C a){float x,y;asm(\"mov.b64 {%0,%1},%2;\":\"=f\"(x),\"=f\"(y):\"l\"(a));return x;}\n"
+             "DI float hi(C a){float x,y;asm(\"mov.b64 {%0,%1},%2;\":\"=f\"(x),\"=f\"(y):\"l\"(a));return y;}\n"
+             "DI C A(C a,C b){C d;asm(\"add.rn.f32x2 %0,%1,%2;\":\"=l\"(d):\"l\"(a),\"l\"(b));return d;}\n"
+             "DI C M(C a,C b){C d;asm(\"mul.rn.f32x2 %0,%1,%2;\":\"=l\"(d):\"l\"(a),\"l\"(b));return d;}\n"
+             "DI C F(C a,C b,C c){C d;asm(\"fma.rn.f32x2 %0,%1,%2,%3;\":\"=l\"(d):\"l\"(a),\"l\"(b),\"l\"(c));return d;}\n"
+             "DI C N(C a){return pk(-lo(a),-hi(a));}\n"
+             "DI C I(C a){return pk(-hi(a),lo(a));}\n"
+             "DI C NI(C a){return pk(hi(a),-lo(a));}\n";
+    }
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << "," << (threads >= 256 ? 2 : 4)
       << ") svpass(C* __restrict__ psi){\n";
     if (multi) o << "extern __shared__ C sm[];\n";
@@ -304,7 +527,8 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
     }
     o << "C v[" << R << "];\nunsigned long long g;\n";
     if (multi) o << "unsigned tl;\n";
-    cd fac = 1;
+    PassState ps;
+    ps.ph.assign(R, cd(1, 0));
     for (size_t si = 0; si < sym.stages.size(); ++si) {
         const StageSym& st = sym.stages[si];
         StageCtx sc;
@@ -343,19 +567,26 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
             for (int s = 0; s < R; ++s) o << reg(s) << "=sm[tl^" << loff[s] << "u];";
             o << "\n";
         }
-        for (const LOp& op : st.ops) emit_op(e, op, sc, fac);
+        for (const LOp& op : st.ops) emit_op(e, op, sc, ps);
         if (si + 1 == sym.stages.size()) {
-            if (!is1(fac)) {
-                o << "// deferred scalar factor of the pass\n";
-                for (int s = 0; s < R; ++s) {
-                    auto mm = mul(e, reg(s), fac);
-                    o << reg(s) << "=mk(" << mm.first << "," << mm.second << ");";
-                }
-                o << "\n";
+            // pending factors of non-register qubits need the index bit: apply them first
+            std::vector<int> rt;
+            for (auto& kv : ps.pend)
+                if (sc.pos[kv.first] < 0) rt.push_back(kv.first);
+            for (int q : rt) emit_flush(e, sc, ps, q);
+            o << "// deferred factors of the pass (scalar, per register qubit, per register)\n";
+            for (int s = 0; s < R; ++s) {
+                cd c = ps.fac * ps.ph[s];
+                for (auto& kv : ps.pend) c *= ((s >> sc.pos[kv.first]) & 1) ? kv.second.second : kv.second.first;
+                if (is1(c)) continue;
+                o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
             }
+            o << "\n";
             for (int s = 0; s < R; ++s) o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
             o << "\n";
         } else {
+            // unit phases are tied to this stage's register numbering: apply before re-distribution
+            for (int s = 0; s < R; ++s) flush_ph(e, ps, s);
             for (int s = 0; s < R; ++s) o << "sm[tl^" << loff[s] << "u]=" << reg(s) << ";";
             o << "\n";
         }
@@ -418,6 +649,15 @@ sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::s
     ce = cudaLibraryGetKernel(&fn, lib, "svpass");
     if (ce == cudaSuccess && smem > 48 * 1024)
         ce = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // ask for the largest shared-memory carve-out so two 64 KiB tiles stay resident per SM
+    // (the default heuristic, and settings made by other libraries in the process, may pick
+    // a smaller one and halve the occupancy)
+    static const int carveout = [] {
+        const char* s = getenv("SV_CARVEOUT");
+        return s ? atoi(s) : -1;
+    }();
+    if (ce == cudaSuccess && smem > 0 && carveout >= 0)
+        ce = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     if (ce != cudaSuccess) {
         err = std::string("cudaLibraryGetKernel/cudaFuncSetAttribute: ") + cudaGetErrorString(ce);
         return SV_ERR_CUDA;

@@ -19,6 +19,7 @@
 // register stages of RB qubits the same way.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
@@ -283,6 +284,25 @@ bool make_sym(const std::vector<const LOp*>& ops, const std::vector<StagePlan>& 
         for (int oi : sp.ops) ss.ops.push_back(*ops[oi]);
         sym.stages.push_back(std::move(ss));
     }
+    // Coalescing: a stage that loads from / stores to HBM must keep the lowest qubits as lane
+    // bits (>= 64 contiguous bytes per lane group).  If the first (last) stage holds one of them
+    // in registers, add an op-free stage that moves the tile through shared memory instead.
+    const int cl = dbl ? 2 : 3;
+    auto bad = [&](const StageSym& s) {
+        for (int q : s.rq)
+            if (q < cl) return true;
+        return false;
+    };
+    auto io_stage = [&]() {
+        StageSym s;
+        for (int b = m - 1; b >= 0 && (int)s.rq.size() < rb; --b)
+            if (sym.tq[b] >= cl) s.rq.push_back(sym.tq[b]);
+        return s;
+    };
+    if (m >= rb + cl) {
+        if (bad(sym.stages.front())) sym.stages.insert(sym.stages.begin(), io_stage());
+        if (bad(sym.stages.back())) sym.stages.push_back(io_stage());
+    }
     return true;
 }
 
@@ -375,6 +395,43 @@ bool write_tile_params(const TileSym& sym, const Context& ctx, PassPlan& pp, std
 
 size_t coef_size(const LOp& op) { return op.coef.size(); }
 
+// Estimated issue cost of an op in the generated kernel, in instructions per amplitude
+// (calibrated on the SASS of generated passes, tools/sass_stats.py).  A pass stays
+// HBM-bound while its total stays below the budget: one pass moves 2 x 2^n x b bytes in
+// the time the SMs issue ~90 instructions per amplitude.
+double op_cost(const LOp& op) {
+    switch (op.kind) {
+        case OP_H: case OP_SX: case OP_SXDG: case OP_SY: case OP_SYDG: return 2.2;
+        case OP_X: case OP_SWAP: return 0.3;
+        case OP_Y: return 0.8;
+        case OP_U1: return 8;
+        case OP_U2: return 16;
+        case OP_U3: return 32;
+        case OP_U4: return 64;
+        case OP_T: case OP_TDG: return 1.3;
+        case OP_Z: case OP_S: case OP_SDG: return 0.6;
+        case OP_PHASE: return 2;
+        case OP_DIAG1: case OP_DIAG2: case OP_SCALAR: return 4;
+        default: return 1;
+    }
+}
+
+bool diag_into_regs() {
+    static bool b = [] {
+        const char* e = getenv("SV_DIAG_REG");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
+double pass_budget() {
+    static double b = [] {
+        const char* e = getenv("SV_PASS_BUDGET");
+        return e ? atof(e) : 110.0;
+    }();
+    return b;
+}
+
 }  // namespace
 
 sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,
@@ -407,6 +464,8 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
         std::vector<int> pass_ops, deferred;
         uint64_t S = lowmask, blocked = 0;
         size_t ncoef = 0;
+        double cost = 0;
+        const double budget = o.use_jit() ? pass_budget() : 1e30;
         const LOp& first = ops[remaining[0]];
         if (first.densek) {
             emit_dense(first);
@@ -417,7 +476,8 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
             const LOp& op = ops[idx];
             const bool full = per_gate ? !pass_ops.empty()
                                        : (pass_ops.size() >= (size_t)kMaxOps ||
-                                          ncoef + coef_size(op) > (size_t)kMaxCoefComplex);
+                                          ncoef + coef_size(op) > (size_t)kMaxCoefComplex ||
+                                          (!pass_ops.empty() && cost + op_cost(op) > budget));
             if (op.densek || full || (op.touched & blocked)) {
                 deferred.push_back(idx);
                 blocked |= op.touched;
@@ -428,6 +488,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                 S = need;
                 pass_ops.push_back(idx);
                 ncoef += coef_size(op);
+                cost += op_cost(op);
             } else {
                 deferred.push_back(idx);
                 blocked |= op.touched;
@@ -439,7 +500,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
         for (size_t i = 0; i < pass_ops.size(); ++i) todo[i] = (int)i;
         std::vector<int> leftover;
         while (!todo.empty()) {
-            if ((int)stages.size() == kMaxStages) {
+            if ((int)stages.size() == kMaxStages - 2) {  // room for the two I/O stages
                 for (int i : todo) leftover.push_back(pass_ops[i]);
                 break;
             }
@@ -465,6 +526,25 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                     sblocked |= op.touched;
                 }
             }
+            if (diag_into_regs()) {
+                // Free register slots go to the stage's most used diagonal qubits and controls:
+                // held in registers they are resolved at compile time instead of by a
+                // per-thread predicate (targets were placed first, so no op is displaced).
+                int cnt[64] = {0};
+                for (int i : sp.ops) {
+                    const LOp& op = ops[pass_ops[i]];
+                    for (int q : op.dq) cnt[q] += 2;
+                    for (int q : op.ctrl) cnt[q] += 1;
+                }
+                while (popc(sp.R) < rb) {
+                    int best = -1;
+                    for (int q = 0; q < 64; ++q)
+                        if (cnt[q] > 0 && !((sp.R >> q) & 1) && ((S >> q) & 1) && (best < 0 || cnt[q] > cnt[best]))
+                            best = q;
+                    if (best < 0) break;
+                    sp.R |= 1ull << best;
+                }
+            }
             stages.push_back(std::move(sp));
             todo = std::move(sdef);
         }
@@ -486,7 +566,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
         const bool ok = dbl ? write_tile_params<double>(*pp.sym, ctx, pp, err)
                             : write_tile_params<float>(*pp.sym, ctx, pp, err);
         if (!ok) return SV_ERR_STATE;
-        out.stages += stages.size();
+        out.stages += pp.sym->stages.size();
         out.passes.push_back(std::move(pp));
         // ---- next round: leftovers and deferred gates in original order
         std::vector<int> next = deferred;

@@ -46,6 +46,8 @@ struct sv_plan_s {
     bool jitted = false;
     svb::Schedule sched;
     uint64_t hbm_bytes = 0;
+    std::vector<cudaEvent_t> prof_ev;   // per-pass timing (opts.profile)
+    int prof_n = 0;
     cudaGraphExec_t graph = nullptr;
     void* graph_ptr = nullptr;
     cudaStream_t graph_stream = nullptr;

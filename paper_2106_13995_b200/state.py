@@ -30,8 +30,9 @@ def _dtype(d) -> int:
 
 
 def make_opts(fuse: bool = True, tile_qubits: int = 0, force_kernel: int = 0, check_unitary: bool = False,
-              use_graph: bool = False) -> RunOpts:
-    return RunOpts(int(fuse), int(tile_qubits), 0, int(force_kernel), int(check_unitary), int(use_graph))
+              use_graph: bool = False, profile: bool = False) -> RunOpts:
+    return RunOpts(int(fuse), int(tile_qubits), 0, int(force_kernel), int(check_unitary), int(use_graph),
+                   int(profile))
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -54,6 +55,14 @@ class Plan:
         g, p, s = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         check(lib.sv_plan_info(self._h, ctypes.byref(n), ctypes.byref(g), ctypes.byref(p), ctypes.byref(s)))
         return {"n": n.value, "gates": g.value, "passes": p.value, "stages": s.value}
+
+    def pass_times(self):
+        """Per-pass device ms of the last apply (plan compiled with profile=True)."""
+        n = ctypes.c_int()
+        check(lib.sv_plan_pass_times(self._h, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_float * max(1, n.value))()
+        check(lib.sv_plan_pass_times(self._h, buf, n.value, ctypes.byref(n)))
+        return list(buf)[: n.value]
 
     def source(self, i: int) -> str:
         """Generated CUDA source of tile pass i (single-GPU schedule)."""

@@ -29,3 +29,12 @@ with P.StateVector(c.n, a.dtype) as sv:
         st = sv.apply_plan(plan)
     sv.sync()
 print(st, plan.info())
+
+# per-pass device times of a back-to-back run (CUDA events between launches)
+pplan = P.Plan(W.to_text(c), a.dtype, fuse=bool(a.fuse), profile=True)
+with P.StateVector(c.n, a.dtype) as sv:
+    for _ in range(3):
+        sv.init_zero()
+        sv.apply_plan(pplan)
+    t = pplan.pass_times()
+    print("pass ms:", " ".join(f"{x:.3f}" for x in t), " total", round(sum(t), 3))
