@@ -1,6 +1,8 @@
 // capi.cpp -- the C-ABI (include/sv.h): handles, init, gate/circuit application, readout.
 #include <algorithm>
 #include <chrono>
+#include <list>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -536,17 +538,39 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
 sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* opts, sv_run_stats* stats) {
     if (!s || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
     const auto t0 = std::chrono::steady_clock::now();
+    // process-wide plan cache keyed by (dtype, options, IR text): a circuit that is run again
+    // skips parsing, planning and code generation (SURVEY 8(b) plan_cache)
+    static std::mutex mu;
+    static std::list<std::pair<std::string, sv_plan_s*>> cache;
+    std::string key(reinterpret_cast<const char*>(&s->dtype), sizeof(s->dtype));
+    sv_run_opts o{};
+    if (opts) o = *opts;
+    key.append(reinterpret_cast<const char*>(&o), sizeof(o));
+    key.append(ir_text);
     sv_plan p = nullptr;
-    sv_status st = sv_plan_compile(ir_text, s->dtype, opts, &p);
-    if (st != SV_OK) return st;
-    if (p->circ.n != s->n) {
-        sv_plan_destroy(p);
-        return fail(SV_ERR_STATE, "circuit width does not match the state");
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& kv : cache)
+            if (kv.first == key) {
+                p = kv.second;
+                break;
+            }
     }
+    sv_status st = SV_OK;
+    if (!p) {
+        st = sv_plan_compile(ir_text, s->dtype, opts, &p);
+        if (st != SV_OK) return st;
+        std::lock_guard<std::mutex> lk(mu);
+        cache.emplace_front(key, p);
+        while (cache.size() > 16) {
+            sv_plan_destroy(cache.back().second);
+            cache.pop_back();
+        }
+    }
+    if (p->circ.n != s->n) return fail(SV_ERR_STATE, "circuit width does not match the state");
     st = sv_plan_apply(s, p, stats);
     const auto t1 = std::chrono::steady_clock::now();
     if (stats) stats->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    sv_plan_destroy(p);
     return st;
 }
 
@@ -591,6 +615,8 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
     std::vector<int> so = lq;
     std::sort(so.begin(), so.end());
     for (int j = 0; j < nql; ++j) P.sorted[j] = so[j];
+    P.smask = 0;
+    for (int j = 0; j < nql; ++j) P.smask |= 1ull << so[j];
     const uint64_t rest = 1ull << (s->nl - nql);
     P.per_chunk = std::min<uint64_t>(rest, 1ull << 13);
     P.chunks = rest / P.per_chunk;

@@ -439,6 +439,27 @@ __global__ void __launch_bounds__(256) marginal_partial_kernel(const typename V2
     if (threadIdx.x == 0) partial[blk] = red[0];
 }
 
+// Wide subsets (many bins, few terms each): one thread per bin k, summing its 2^(n-nq)
+// amplitudes sequentially in rest-index order (deterministic).  Consecutive threads own
+// consecutive k, so a warp reads 32 neighbouring amplitudes per step when the subset holds
+// the low qubits.
+template <typename real>
+__global__ void __launch_bounds__(256) marginal_bin_kernel(const typename V2<real>::t* __restrict__ psi,
+                                                           MarginalParams P, uint64_t rest, double* __restrict__ out) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >> P.nq) return;
+    uint64_t kbits = 0;
+    for (int j = 0; j < P.nq; ++j) kbits |= ((k >> j) & 1ull) << P.q[j];
+    double acc = 0.0;
+    uint64_t cur = 0;  // rest bits deposited at the non-subset positions, in increasing order
+    for (uint64_t r = 0; r < rest; ++r) {
+        const auto a = psi[cur | kbits];
+        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+        cur = ((cur | P.smask) + 1) & ~P.smask;
+    }
+    out[k] = acc;
+}
+
 __global__ void __launch_bounds__(256) marginal_final_kernel(const double* __restrict__ partial, uint64_t chunks,
                                                              double* __restrict__ out) {
     __shared__ double red[256];
@@ -525,6 +546,16 @@ cudaError_t launch_fill(bool dbl, void* psi, uint64_t N, double re, double im, c
 cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, double* partial, double* out,
                             cudaStream_t st) {
     const uint64_t nk = 1ull << P.nq;
+    if (P.nq >= 12) {
+        const uint64_t rest = P.chunks * P.per_chunk;
+        const unsigned grid = (unsigned)((nk + 255) / 256);
+        if (dbl)
+            marginal_bin_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(psi), P, rest, out);
+        else
+            marginal_bin_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(psi), P, rest, out);
+        (void)partial;
+        return cudaGetLastError();
+    }
     const uint64_t blocks = nk * P.chunks;
     const int threads = P.per_chunk >= 256 ? 256 : (int)P.per_chunk;
     if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;

@@ -28,6 +28,7 @@ struct MarginalParams {
     int nq;
     int q[28];             // subset qubits (bit j of k <-> q[j])
     int sorted[28];        // subset qubits ascending
+    uint64_t smask;        // bit mask of the subset qubits
     uint64_t chunks;       // chunks of the rest space per k
     uint64_t per_chunk;    // rest indices per chunk
 };

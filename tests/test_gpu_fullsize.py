@@ -1,0 +1,71 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (default
+plan: fused generated passes, m = 13/12 tile qubits, 256 threads), via properties that hold at
+any size or outputs the oracle computes one by one (SURVEY 8(c) comparison procedure)."""
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import U_C64, U_C128, assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2106_13995_b200 as P
+    return P
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_30q_supremacy_mirror(P, dtype):
+    """Config 3 at full width: C then C^dagger returns |0>, norm preserved."""
+    c = W.supremacy(6, 5, 20, seed=0)
+    mirror = W.concat(c, W.inverse(c))
+    G = W.gate_count(mirror)
+    u = U_C64 if dtype == "c64" else U_C128
+    with P.StateVector(30, dtype) as sv:
+        st = sv.apply_plan(P.Plan(W.to_text(c), dtype))
+        assert abs(sv.norm() - 1) <= 8 * W.gate_count(c) * u
+        sv.apply_plan(P.Plan(W.to_text(W.inverse(c)), dtype))
+        a0 = complex(sv.amplitudes(0, 1)[0])
+        head = sv.amplitudes(1, 1 << 16)
+        nrm = sv.norm()
+    assert st["passes"] <= 16
+    assert abs(a0 - 1) <= 8 * G * u
+    assert np.max(np.abs(head)) <= 8 * G * u
+    assert abs(nrm - 1) <= 8 * G * u
+
+
+def test_24q_supremacy_d20_full_state_vs_oracle(P):
+    """Same circuit family, depth and launch configuration, at a width the oracle finishes."""
+    c = W.supremacy(6, 4, 20, seed=1)
+    text = W.to_text(c)
+    ref = oracle.simulate(text)
+    for dtype in ("c64", "c128"):
+        with P.StateVector(24, dtype) as sv:
+            st = sv.apply_circuit(text)
+            got = sv.amplitudes()
+        assert st["passes"] >= 2  # several tiles per pass and several passes
+        assert_close(got, ref, dtype, W.gate_count(c))
+
+
+def test_31q_multiplier_basis_exact(P):
+    """Config 4 at full width (8x7 multiplier, c64): basis inputs map exactly to the oracle's
+    classical image (bit-level evaluator), amplitude exactly 1, norm exactly 1 (R10)."""
+    c = W.multiplier(8, 7)
+    text = W.to_text(c)
+    rng = np.random.default_rng(31)
+    xs = [int(x) for x in rng.integers(0, 1 << 31, 6, dtype=np.int64)]
+    xs += [255 | (127 << 8)]  # a = 255, b = 127, empty product register
+    ys = oracle.classical_map(text, np.array(xs, dtype=np.uint64))
+    plan = P.Plan(text, "c64")
+    with P.StateVector(31, "c64") as sv:
+        for x, y in zip(xs, ys.tolist()):
+            sv.init_basis(x)
+            sv.apply_plan(plan)
+            assert sv.amplitudes(int(y), 1)[0] == 1 + 0j, (x, y)
+            assert sv.norm() == 1.0
+    a, b = 255, 127
+    assert int(ys[-1]) == a | (b << 8) | ((a * b) << 15)
