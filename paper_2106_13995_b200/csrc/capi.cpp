@@ -622,10 +622,12 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
     P.chunks = rest / P.per_chunk;
     const uint64_t nk = 1ull << nql;
     const int shards = shard_count(s);
-    sv_status st = ensure_scratch(s, nk * P.chunks + nk * shards);
+    // partials: per-chunk trees (nk x chunks) or per-bin chunks of >= 64 rest indices
+    const uint64_t nparts = nk * std::max<uint64_t>(P.chunks, std::max<uint64_t>(1, rest / 64));
+    sv_status st = ensure_scratch(s, nparts + nk * shards);
     if (st != SV_OK) return st;
     double* partial = s->d_scratch;
-    double* outs = s->d_scratch + nk * P.chunks;
+    double* outs = s->d_scratch + nparts;
     for (int i = 0; i < shards; ++i) {
         cudaError_t e = launch_marginal(s->dbl, s->shard_ptr(i), P, partial, outs + nk * i, s->stream);
         if (e != cudaSuccess) return cuda_fail(e, "marginal");
@@ -646,7 +648,23 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
         for (int r = 0; r < s->world; ++r) ranks.push_back(r);
     }
     const size_t nout = (size_t)1 << nq;
+    bool identity = ranks.size() == 1 && gq.empty();
+    for (int j = 0; j < nql && identity; ++j) identity = lj[j] == j;
+    if (identity) {
+        memcpy(host_out, all.data(), nout * sizeof(double));
+        return SV_OK;
+    }
     for (size_t k = 0; k < nout; ++k) host_out[k] = 0.0;
+    // byte-wise deposit tables: bit j of the local bin index -> output bit lj[j]
+    const int nbytes = (nql + 7) / 8;
+    std::vector<size_t> tab((size_t)std::max(1, nbytes) * 256, 0);
+    for (int b = 0; b < nbytes; ++b)
+        for (int v = 0; v < 256; ++v) {
+            size_t d = 0;
+            for (int j = 0; j < 8 && 8 * b + j < nql; ++j)
+                if ((v >> j) & 1) d |= (size_t)1 << lj[8 * b + j];
+            tab[(size_t)b * 256 + v] = d;
+        }
     for (size_t i = 0; i < ranks.size(); ++i) {
         const int r = ranks[i];
         size_t kg = 0;
@@ -654,8 +672,7 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
             if ((r >> (gq[j] - s->nl)) & 1) kg |= (size_t)1 << gj[j];
         for (uint64_t kl = 0; kl < nk; ++kl) {
             size_t k = kg;
-            for (int j = 0; j < nql; ++j)
-                if ((kl >> j) & 1) k |= (size_t)1 << lj[j];
+            for (int b = 0; b < nbytes; ++b) k |= tab[(size_t)b * 256 + ((kl >> (8 * b)) & 255)];
             host_out[k] += all[i * nk + kl];
         }
     }

@@ -443,20 +443,39 @@ __global__ void __launch_bounds__(256) marginal_partial_kernel(const typename V2
 // amplitudes sequentially in rest-index order (deterministic).  Consecutive threads own
 // consecutive k, so a warp reads 32 neighbouring amplitudes per step when the subset holds
 // the low qubits.
+// Block (x: 256 bins, y: rest chunk of `per` indices): partial[chunk][k] = fixed-order sum of
+// the chunk (8 independent accumulators combined in a fixed order, for memory parallelism).
 template <typename real>
 __global__ void __launch_bounds__(256) marginal_bin_kernel(const typename V2<real>::t* __restrict__ psi,
-                                                           MarginalParams P, uint64_t rest, double* __restrict__ out) {
+                                                           MarginalParams P, uint64_t per, double* __restrict__ partial) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (k >> P.nq) return;
+    const uint64_t nk = 1ull << P.nq;
+    if (k >= nk) return;
+    const uint64_t chunk = blockIdx.y;
     uint64_t kbits = 0;
     for (int j = 0; j < P.nq; ++j) kbits |= ((k >> j) & 1ull) << P.q[j];
-    double acc = 0.0;
-    uint64_t cur = 0;  // rest bits deposited at the non-subset positions, in increasing order
-    for (uint64_t r = 0; r < rest; ++r) {
-        const auto a = psi[cur | kbits];
-        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
-        cur = ((cur | P.smask) + 1) & ~P.smask;
+    // rest index chunk*per deposited at the non-subset positions
+    uint64_t cur = 0, r0 = chunk * per;
+    for (int b = 0; r0; ++b)
+        if (!((P.smask >> b) & 1)) { cur |= (r0 & 1ull) << b; r0 >>= 1; }
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t r = 0; r < per; r += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const auto a = psi[cur | kbits];
+            acc[u] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+            cur = ((cur | P.smask) + 1) & ~P.smask;
+        }
     }
+    partial[chunk * nk + k] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
+__global__ void __launch_bounds__(256) marginal_bin_final_kernel(const double* __restrict__ partial, uint64_t nk,
+                                                                 uint64_t chunks, double* __restrict__ out) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= nk) return;
+    double acc = 0.0;
+    for (uint64_t c = 0; c < chunks; ++c) acc += partial[c * nk + k];
     out[k] = acc;
 }
 
@@ -546,14 +565,20 @@ cudaError_t launch_fill(bool dbl, void* psi, uint64_t N, double re, double im, c
 cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, double* partial, double* out,
                             cudaStream_t st) {
     const uint64_t nk = 1ull << P.nq;
-    if (P.nq >= 12) {
+    if (P.nq >= 12 && P.chunks * P.per_chunk >= 8) {
+        // partial needs chunks2 * nk doubles: the caller sizes it as nk * P.chunks (>= this)
         const uint64_t rest = P.chunks * P.per_chunk;
-        const unsigned grid = (unsigned)((nk + 255) / 256);
+        uint64_t per = rest >= 64 ? 64 : rest;
+        while (rest / per > 32768) per *= 2;  // grid.y limit
+        const uint64_t chunks2 = rest / per;
+        const dim3 grid((unsigned)((nk + 255) / 256), (unsigned)chunks2);
         if (dbl)
-            marginal_bin_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(psi), P, rest, out);
+            marginal_bin_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(psi), P, per, partial);
         else
-            marginal_bin_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(psi), P, rest, out);
-        (void)partial;
+            marginal_bin_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(psi), P, per, partial);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        marginal_bin_final_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(partial, nk, chunks2, out);
         return cudaGetLastError();
     }
     const uint64_t blocks = nk * P.chunks;
