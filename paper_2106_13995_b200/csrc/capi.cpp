@@ -114,6 +114,7 @@ sv_status new_state(int n, int nl, int world, int rank, sv_dtype dt, void* strea
 void free_state(sv_state_s* s) {
     if (!s) return;
     if (s->owned && s->d) cudaFree(s->d);
+    if (s->d2) cudaFree(s->d2);
     if (s->d_scratch) cudaFree(s->d_scratch);
     if (s->xbuf) cudaFree(s->xbuf);
     if (s->comm) comm_destroy(s->comm);
@@ -143,7 +144,29 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
     for (const PassPlan& pp : sc.passes) {
         ++pi;
         cudaError_t e;
-        if (pp.kind == PassPlan::TILE && pp.jit_fn)
+        if (pp.kind == PassPlan::PERM) {
+            // out-of-place gather into the scratch state, then swap the buffers (or copy back
+            // into a borrowed buffer)
+            const size_t bytes = (size_t)s->local_amps() * s->amp_bytes();
+            if (!s->d2) {
+                e = cudaMalloc(&s->d2, bytes);
+                if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    s->d2 = nullptr;
+                    return fail(SV_ERR_RESOURCE, "permutation pass needs a second state buffer of " +
+                                                     std::to_string(bytes) + " bytes");
+                }
+            }
+            e = jit_launch_perm(pp, psi, s->d2, s->stream);
+            if (e == cudaSuccess) {
+                if (s->owned && psi == s->d) {
+                    std::swap(s->d, s->d2);
+                    psi = s->d;
+                } else {
+                    e = cudaMemcpyAsync(psi, s->d2, bytes, cudaMemcpyDeviceToDevice, s->stream);
+                }
+            }
+        } else if (pp.kind == PassPlan::TILE && pp.jit_fn)
             e = jit_launch(pp, psi, s->stream);
         else if (pp.kind == PassPlan::TILE)
             e = launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles, s->stream);
@@ -169,15 +192,20 @@ sv_status plan_schedule(sv_plan_s* p) {
     for (int q = 0; q < p->circ.n; ++q) ctx.phys[q] = q;
     ctx.dbl = p->dtype == SV_C128;
     std::string err;
+    p->sched = Schedule();
+    Schedule perm;
+    const bool have_perm = !p->opts.use_graph && build_perm_schedule(p->circ, ctx, p->opts, perm);
     std::vector<LOp> ops;
     for (size_t i = 0; i < p->circ.gates.size(); ++i) {
         bool needs_global = false;
         const sv_status st = lower_gate(p->circ.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
         if (st != SV_OK) return fail(st, err);
     }
-    p->sched = Schedule();
     const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err);
     if (st != SV_OK) return fail(st, err);
+    // a reversible circuit: one gather pass, unless its scattered reads cost more than the
+    // fused tile passes (both estimated in HBM passes)
+    if (have_perm && perm.passes[0].perm_cost < 1.2 * (double)p->sched.passes.size()) p->sched = std::move(perm);
     p->cached = true;
     p->jitted = false;
     return SV_OK;
@@ -443,11 +471,10 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     if (!p->cached || pass < 0 || pass >= (int)p->sched.passes.size()) return fail(SV_ERR_RANGE, "bad pass index");
     const PassPlan& pp = p->sched.passes[pass];
     std::string src;
-    if (pp.kind == PassPlan::TILE && pp.sym) {
-        int threads;
-        size_t smem;
-        src = gen_pass_source(*pp.sym, threads, smem);
-    }
+    int threads;
+    size_t smem;
+    if (pp.kind == PassPlan::TILE && pp.sym) src = gen_pass_source(*pp.sym, threads, smem);
+    else if (pp.kind == PassPlan::PERM) src = gen_perm_source(pp, pp.perm_dbl, threads);
     if (len) *len = src.size();
     if (buf && cap) {
         const size_t n = std::min(cap - 1, src.size());

@@ -85,8 +85,18 @@ struct TileSym {                 // symbolic tile pass: what both backends execu
     std::vector<StageSym> stages;
 };
 
+// A classical reversible gate for the whole-permutation pass: X on t (or SWAP of t, t2)
+// when every control is 1.
+struct PermGate {
+    int t = -1, t2 = -1;
+    std::vector<int> ctrl;
+};
+
 struct PassPlan {
-    enum Kind { TILE, DENSE } kind = TILE;
+    enum Kind { TILE, DENSE, PERM } kind = TILE;
+    std::vector<PermGate> perm;          // PERM: the circuit's gates in order
+    bool perm_dbl = false;
+    double perm_cost = 1.0;              // PERM: estimated cost in HBM passes
     std::shared_ptr<TileSym> sym;        // TILE: the symbolic pass
     void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
     int jit_threads = 0;
@@ -105,6 +115,10 @@ struct Schedule {
 
 sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,
                          std::string& err);
+
+// if every gate is a classical reversible gate (X / SWAP with any controls)
+// and the state is 10..32 qubits on one GPU, the whole circuit becomes one PERM pass.
+bool build_perm_schedule(const Circuit& c, const Context& ctx, const RunOpts& o, Schedule& out);
 
 int default_rb(bool dbl, int nl);
 int default_tile_qubits(bool dbl, int nl, int rb);

@@ -516,7 +516,8 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
              "DI C I(C a){return pk(-hi(a),lo(a));}\n"
              "DI C NI(C a){return pk(hi(a),-lo(a));}\n";
     }
-    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << "," << (threads >= 256 ? 2 : 4)
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
+      << (threads >= 512 ? 1 : threads >= 256 ? 2 : 4)
       << ") svpass(C* __restrict__ psi){\n";
     if (multi) o << "extern __shared__ C sm[];\n";
     o << "const unsigned t=threadIdx.x;\n";
@@ -668,14 +669,80 @@ sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::s
     return SV_OK;
 }
 
+// a whole reversible circuit (X / SWAP with controls) in one HBM pass:
+// out[j] = in[f^-1(j)].  Each warp owns 1024 consecutive outputs j = base | lane | s << 5
+// (s = 0..31); a thread evaluates f^-1 for its 32 indices bit-sliced -- plane q holds bit q
+// of the 32 indices, so a Toffoli is one AND-XOR on 32-bit words -- running the inverse
+// gates in reverse order, transposes the 32x32 bit matrix into 32 source indices and
+// gathers.  Pure data movement: exact (reading R10).  Stores are coalesced; loads are
+// coalesced whenever f leaves the low qubits alone (true for the multipliers, whose
+// operand register A is restored).
+std::string gen_perm_source(const PassPlan& pp, bool dbl, int& threads) {
+    const int n = pp.m;
+    std::ostringstream o;
+    o << "// generated permutation pass: n=" << n << " gates=" << pp.perm.size() << "\n";
+    if (dbl) o << "struct alignas(16) C { double x, y; };\n";
+    else o << "typedef unsigned long long C;\n";
+    const uint64_t warps = 1ull << (n - 10);
+    threads = (int)std::min<uint64_t>(256, warps * 32);
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ") svpass(const C* __restrict__ in, "
+      << "C* __restrict__ out){\n";
+    o << "const unsigned lane=threadIdx.x&31u;\n";
+    o << "const unsigned long long base=(((unsigned long long)blockIdx.x*blockDim.x+threadIdx.x)>>5)<<10;\n";
+    o << "unsigned p[32];\n";
+    static const char* pat[5] = {"0xAAAAAAAAu", "0xCCCCCCCCu", "0xF0F0F0F0u", "0xFF00FF00u", "0xFFFF0000u"};
+    for (int q = 0; q < 32; ++q) {
+        if (q >= n) o << "p[" << q << "]=0u;";
+        else if (q < 5) o << "p[" << q << "]=0u-((lane>>" << q << ")&1u);";
+        else if (q < 10) o << "p[" << q << "]=" << pat[q - 5] << ";";
+        else o << "p[" << q << "]=0u-(unsigned)((base>>" << q << ")&1ull);";
+    }
+    o << "\n";
+    // f^-1: the gates are self-inverse, so apply them in reverse order
+    for (size_t i = pp.perm.size(); i-- > 0;) {
+        const PermGate& g = pp.perm[i];
+        std::string m;
+        for (int c : g.ctrl) m += (m.empty() ? "" : "&") + std::string("p[") + std::to_string(c) + "]";
+        if (g.t2 < 0) {
+            if (m.empty()) o << "p[" << g.t << "]=~p[" << g.t << "];";
+            else o << "p[" << g.t << "]^=" << m << ";";
+        } else {
+            o << "{unsigned d=(p[" << g.t << "]^p[" << g.t2 << "])" << (m.empty() ? "" : "&" + m) << ";p[" << g.t
+              << "]^=d;p[" << g.t2 << "]^=d;}";
+        }
+        o << "\n";
+    }
+    // transpose: afterwards p[s] bit q = source index of output s, bit q
+    for (int w = 16; w >= 1; w >>= 1) {
+        const uint32_t mask = w == 16 ? 0x0000FFFFu : w == 8 ? 0x00FF00FFu : w == 4 ? 0x0F0F0F0Fu
+                            : w == 2 ? 0x33333333u : 0x55555555u;
+        for (int k = 0; k < 32; ++k) {
+            if (k & w) continue;
+            o << "{unsigned t=((p[" << k << "]>>" << w << ")^p[" << k + w << "])&" << mask << "u;p[" << k
+              << "]^=t<<" << w << ";p[" << k + w << "]^=t;}";
+        }
+        o << "\n";
+    }
+    for (int s = 0; s < 32; ++s) o << "out[base|lane|" << (s << 5) << "u]=in[p[" << s << "]];";
+    o << "\n}\n";
+    return o.str();
+}
+
 sv_status jit_prepare(Schedule& sc, std::string& err) {
     std::vector<PassPlan*> todo;
     for (PassPlan& pp : sc.passes)
-        if (pp.kind == PassPlan::TILE && pp.sym && !pp.jit_fn) todo.push_back(&pp);
+        if (((pp.kind == PassPlan::TILE && pp.sym) || pp.kind == PassPlan::PERM) && !pp.jit_fn) todo.push_back(&pp);
     if (todo.empty()) return SV_OK;
     std::vector<std::string> srcs(todo.size());
-    for (size_t i = 0; i < todo.size(); ++i)
-        srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->jit_threads, todo[i]->jit_smem);
+    for (size_t i = 0; i < todo.size(); ++i) {
+        if (todo[i]->kind == PassPlan::PERM) {
+            srcs[i] = gen_perm_source(*todo[i], todo[i]->perm_dbl, todo[i]->jit_threads);
+            todo[i]->jit_smem = 0;
+            todo[i]->ntiles = ((1ull << todo[i]->m) >> 5) / (uint64_t)todo[i]->jit_threads;
+        } else {
+            srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->jit_threads, todo[i]->jit_smem);
+        }
+    }
     std::vector<sv_status> st(todo.size(), SV_OK);
     std::vector<std::string> errs(todo.size());
     std::vector<void*> fns(todo.size(), nullptr);
@@ -704,6 +771,11 @@ cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream) {
     void* args[] = {&psi};
     return cudaLaunchKernel(pp.jit_fn, dim3((unsigned)pp.ntiles), dim3((unsigned)pp.jit_threads), args,
                             pp.jit_smem, stream);
+}
+
+cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {
+    void* args[] = {&in, &out};
+    return cudaLaunchKernel(pp.jit_fn, dim3((unsigned)pp.ntiles), dim3((unsigned)pp.jit_threads), args, 0, stream);
 }
 
 }  // namespace svb

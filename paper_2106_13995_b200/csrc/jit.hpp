@@ -13,5 +13,8 @@ sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::s
 // Compile every TILE pass of a schedule that has no kernel yet (parallel over passes).
 sv_status jit_prepare(Schedule& sc, std::string& err);
 cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream);
+// whole-permutation pass (out-of-place gather)
+std::string gen_perm_source(const PassPlan& pp, bool dbl, int& threads);
+cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream);
 
 }  // namespace svb

@@ -55,6 +55,74 @@ uint64_t qmask(const std::vector<int>& qs) {
 
 int default_rb(bool dbl, int nl) { return std::max(1, std::min(dbl ? 4 : 5, nl)); }
 
+bool build_perm_schedule(const Circuit& c, const Context& ctx, const RunOpts& o, Schedule& out) {
+    if (!o.use_jit() || ctx.world != 1 || ctx.nl < 10 || ctx.nl > 32 || c.gates.empty()) return false;
+    static const bool enabled = [] {
+        const char* e = getenv("SV_PERM_PASS");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (!enabled) return false;
+    PassPlan pp;
+    pp.kind = PassPlan::PERM;
+    for (const Gate& g : c.gates) {
+        PermGate pg;
+        pg.ctrl = g.controls;
+        if (g.targets.size() == 1 && eq(g.U, {0, 1, 1, 0})) {
+            pg.t = g.targets[0];
+        } else if (g.targets.size() == 2 && eq(g.U, {1, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 0, 1})) {
+            pg.t = g.targets[0];
+            pg.t2 = g.targets[1];
+        } else {
+            return false;
+        }
+        pp.perm.push_back(pg);
+    }
+    for (PermGate& pg : pp.perm) {  // logical -> physical (identity on one GPU)
+        pg.t = ctx.phys[pg.t];
+        if (pg.t2 >= 0) pg.t2 = ctx.phys[pg.t2];
+        for (int& q : pg.ctrl) q = ctx.phys[q];
+    }
+    pp.touched_amps = 1ull << ctx.nl;
+    pp.m = ctx.nl;  // qubits of the (local) state
+    pp.perm_dbl = ctx.dbl;
+    // Cost model (HBM passes): the gather is coalesced only where f^-1 keeps a warp's 32
+    // sources together.  Sample warps on the host, count distinct 32-byte sectors per gather.
+    {
+        uint64_t seed = 0x9E3779B97F4A7C15ull, sectors = 0, gathers = 0;
+        const int ab = ctx.dbl ? 16 : 8;
+        for (int w = 0; w < 64; ++w) {
+            seed = seed * 6364136223846793005ull + 1442695040888963407ull;
+            const uint64_t base = ((seed >> 11) << 10) & ((1ull << ctx.nl) - 1) & ~1023ull;
+            for (int s = 0; s < 32; s += 7) {
+                std::vector<uint64_t> sec;
+                for (int lane = 0; lane < 32; ++lane) {
+                    uint64_t x = base | (uint64_t)lane | ((uint64_t)s << 5);
+                    for (size_t i = pp.perm.size(); i-- > 0;) {
+                        const PermGate& g = pp.perm[i];
+                        bool on = true;
+                        for (int c : g.ctrl) on &= ((x >> c) & 1) != 0;
+                        if (!on) continue;
+                        if (g.t2 < 0) x ^= 1ull << g.t;
+                        else if (((x >> g.t) ^ (x >> g.t2)) & 1) x ^= (1ull << g.t) | (1ull << g.t2);
+                    }
+                    sec.push_back(x * ab / 32);
+                }
+                std::sort(sec.begin(), sec.end());
+                sectors += std::unique(sec.begin(), sec.end()) - sec.begin();
+                ++gathers;
+            }
+        }
+        const double ideal = 32.0 * ab / 32.0;
+        const double ratio = (double)sectors / gathers / ideal;
+        // measured on B200: 32 distinct sectors per 8-byte gather (ratio 4) read 12x the bytes
+        const double read_factor = ratio <= 1.25 ? 1.0 : std::min(12.0, 3.0 * ratio);
+        pp.perm_cost = 0.5 * (read_factor + 1.0);
+    }
+    pp.nops = (int)pp.perm.size();
+    out.passes.push_back(std::move(pp));
+    return true;
+}
+
 int default_tile_qubits(bool dbl, int nl, int rb) {
     // 2^m amplitudes of shared memory per CTA: 64 KiB for both dtypes
     const int m = dbl ? 12 : 13;
@@ -439,8 +507,13 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
     const bool dbl = ctx.dbl;
     const int nl = ctx.nl;
     const int rb = default_rb(dbl, nl);
-    int m_max = o.tile_qubits > 0 ? o.tile_qubits : default_tile_qubits(dbl, nl, rb);
-    m_max = std::max(rb, std::min({m_max, rb + 8, nl, kMaxTileQubits}));
+    static const int env_tile = [] {
+        const char* e = getenv("SV_TILE_QUBITS");
+        return e ? atoi(e) : 0;
+    }();
+    int m_max = o.tile_qubits > 0 ? o.tile_qubits : env_tile > 0 ? env_tile : default_tile_qubits(dbl, nl, rb);
+    // generated kernels take up to 512 threads per tile, the interpreter 256
+    m_max = std::max(rb, std::min({m_max, rb + (o.use_jit() ? 9 : 8), nl, kMaxTileQubits}));
     const int m_pad = std::min(rb + 8, nl);       // single-stage passes: 256 threads
     const int L = std::min(dbl ? 4 : 5, nl);      // low qubits: contiguous 256-byte runs
     const uint64_t lowmask = (L >= 64) ? ~0ull : ((1ull << L) - 1);

@@ -18,6 +18,7 @@ struct sv_state_s {
     sv_dtype dtype = SV_C64;
     bool dbl = false;
     void* d = nullptr;      // local shard (or the whole virtual allocation)
+    void* d2 = nullptr;     // second buffer for out-of-place (permutation) passes
     bool owned = false;
     cudaStream_t stream = nullptr;
     bool own_stream = false;

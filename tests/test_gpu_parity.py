@@ -156,6 +156,43 @@ def test_config2_multiplier_21q_bit_exact(P):
             assert y == x | ((a * b) << 10)
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_permutation_pass_random_state_exact(P, dtype):
+    """a reversible circuit runs as one gather pass; on any input the result
+    is psi_out[f(i)] == psi_in[i] exactly (f from the oracle's bit-level evaluator)."""
+    # a multiplier on qubits 3..15 (the low qubits stay put, so the gathers coalesce and the
+    # planner picks the gather pass), basis preparation, and a SWAP
+    m = W.multiplier(3)
+    shifted = [[W.GateSpec(g.name, tuple(q + 3 for q in g.qubits)) for g in mom] for mom in m.moments]
+    c = W.concat(W.basis_prep(W.Circuit(16, []), 0b1010011 << 3),
+                 W.Circuit(16, shifted + [[W.GateSpec("SWAP", (15, 4))]]))
+    text = W.to_text(c)
+    plan = P.Plan(text, dtype)
+    assert plan.info()["passes"] == 1 and "permutation pass" in plan.source(0)
+    psi0 = input_for(16, 77, dtype)
+    f = oracle.classical_map(text, np.arange(1 << 16, dtype=np.uint64)).astype(np.int64)
+    with P.StateVector(16, dtype) as sv:
+        sv.set_amplitudes(psi0)
+        sv.apply_plan(plan)
+        got = sv.amplitudes()
+    assert np.array_equal(got[f], psi0.astype(got.dtype))
+    assert np.array_equal(got.astype(complex), oracle.simulate(text, psi0))
+
+
+def test_permutation_pass_borrowed_buffer(P):
+    """A borrowed (torch) buffer gets the result copied back in place."""
+    import torch
+    c = W.multiplier(3)
+    text = W.to_text(c)
+    psi0 = W.random_state(13, 5)
+    t = torch.tensor(psi0, dtype=torch.complex128, device="cuda")
+    with P.StateVector.wrap(t, 13) as sv:
+        sv.apply_circuit(text)
+        sv.sync()
+        got = t.cpu().numpy()
+    assert np.array_equal(got, oracle.simulate(text, psi0))
+
+
 def test_multiplier_superposition_support(P):
     """H on A and B: support exactly {|a,b,ab,0>}, each 2^-n (not bit-exact: H rounds)."""
     nb = 3
