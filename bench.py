@@ -261,6 +261,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2106_13995_b200 as P
+    from paper_2106_13995_b200.dist import max_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -318,9 +319,7 @@ def run_ours(args):
     total_ms = sum(step_ms)
     tpass_ms = sum(pass_ms)
     if world > 1:
-        t = torch.tensor([total_ms, tpass_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, tpass_ms = float(t[0]), float(t[1])
+        total_ms, tpass_ms = max_over_ranks([total_ms, tpass_ms])
     ms_per_step = total_ms / args.steps
     value = world * G / (ms_per_step / 1e3)
     amp = 16 if args.dtype == "c128" else 8
@@ -344,9 +343,7 @@ def run_ours(args):
         probs = sv.probabilities(e2e_q)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+        (e2e_s,) = max_over_ranks([e2e_s])
     assert abs(probs.sum() - 1.0) < 1e-3
 
     cpu = None

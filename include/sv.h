@@ -147,6 +147,11 @@ sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uin
 sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len);
 sv_status sv_plan_destroy(sv_plan p);
 
+/* Host-only dry run of the sharded schedule of a plan over `world` GPUs (power of two >= 2),
+ * starting from the identity qubit map: number of global<->local exchange steps, of pass
+ * batches, and of passes rank 0 launches.  No GPU needed. */
+sv_status sv_plan_shard_info(sv_plan p, int world, uint64_t* swaps, uint64_t* batches, uint64_t* passes);
+
 /* Apply a compiled plan to a state (asynchronous).  stats may be NULL. */
 sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats);
 

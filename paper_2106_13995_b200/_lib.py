@@ -64,6 +64,7 @@ def _load():
         "sv_plan_source": (i, [vp, i, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "sv_plan_apply": (i, [vp, vp, ctypes.POINTER(RunStats)]),
         "sv_plan_pass_times": (i, [vp, ctypes.POINTER(ctypes.c_float), i, ip]),
+        "sv_plan_shard_info": (i, [vp, i, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]),
         "sv_apply_circuit": (i, [vp, cp, ctypes.POINTER(RunOpts), ctypes.POINTER(RunStats)]),
         "sv_amplitudes": (i, [vp, u64, u64, vp]),
         "sv_probabilities": (i, [vp, ip, i, dp]),
@@ -87,7 +88,7 @@ lib = _load()
 EXPORTED = ["sv_memory_estimate", "sv_create", "sv_wrap", "sv_nccl_unique_id", "sv_create_sharded",
             "sv_create_virtual_sharded", "sv_destroy", "sv_init_zero", "sv_init_basis", "sv_init_uniform",
             "sv_set_amplitudes", "sv_apply_gate", "sv_plan_compile", "sv_plan_info", "sv_plan_source",
-            "sv_plan_destroy", "sv_plan_pass_times",
+            "sv_plan_destroy", "sv_plan_pass_times", "sv_plan_shard_info",
             "sv_plan_apply", "sv_apply_circuit", "sv_amplitudes", "sv_probabilities", "sv_norm", "sv_sync",
             "sv_info", "sv_device_ptr", "sv_stream", "sv_qubit_map", "sv_last_error", "sv_version"]
 

@@ -484,6 +484,33 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     return SV_OK;
 }
 
+sv_status sv_plan_shard_info(sv_plan p, int world, uint64_t* swaps, uint64_t* batches, uint64_t* passes) {
+    if (!p) return fail(SV_ERR_ARG, "NULL plan");
+    if (world < 2 || (world & (world - 1))) return fail(SV_ERR_ARG, "world must be a power of two >= 2");
+    int g = 0;
+    while ((1 << g) < world) ++g;
+    const int n = p->circ.n, nl = n - g;
+    if (nl < g + 1) return fail(SV_ERR_RANGE, "too few qubits for this world size");
+    std::vector<int> phys(n);
+    for (int q = 0; q < n; ++q) phys[q] = q;
+    RunOpts o = p->opts;
+    if (o.force_kernel == SV_KERNEL_DENSE) o.force_kernel = SV_KERNEL_PER_GATE;
+    ShardPlan sp;
+    std::string err;
+    const sv_status st = shard_plan(p->circ, o, n, nl, world, p->dtype == SV_C128, {0}, phys, sp, err);
+    if (st != SV_OK) return fail(st, err);
+    uint64_t nb = 0, np = 0;
+    for (const ShardStep& s : sp.steps)
+        if (!s.exchange) {
+            ++nb;
+            np += s.sched[0].passes.size();
+        }
+    if (swaps) *swaps = sp.swaps;
+    if (batches) *batches = nb;
+    if (passes) *passes = np;
+    return SV_OK;
+}
+
 sv_status sv_plan_pass_times(sv_plan p, float* ms_out, int cap, int* n) {
     if (!p) return fail(SV_ERR_ARG, "NULL plan");
     if (n) *n = p->prof_n;

@@ -49,6 +49,29 @@ LOp phys_swap(int a, int b) {
     return op;
 }
 
+// launch one shard's schedule
+sv_status run_sched(sv_state_s* s, int i, const Schedule& sc, sv_run_stats* st, std::string& err) {
+    void* psi = s->shard_ptr(i);
+    for (const PassPlan& pp : sc.passes) {
+        cudaError_t e = (pp.kind == PassPlan::TILE && pp.jit_fn) ? jit_launch(pp, psi, s->stream)
+                        : pp.kind == PassPlan::TILE
+                            ? launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles,
+                                               s->stream)
+                            : launch_dense_k(s->dbl, psi, pp.params.data(), pp.groups, s->stream);
+        if (e != cudaSuccess) {
+            err = std::string("pass launch: ") + cudaGetErrorString(e);
+            return SV_ERR_CUDA;
+        }
+        if (st && i == 0) {
+            st->passes++;
+            st->launches++;
+            st->stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
+            st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+        }
+    }
+    return SV_OK;
+}
+
 sv_status run_ops(sv_state_s* s, std::vector<std::vector<LOp>>& ops, const RunOpts& o, sv_run_stats* st,
                   std::string& err) {
     for (int i = 0; i < nshards(s); ++i) {
@@ -110,14 +133,7 @@ sv_status exchange_all(sv_state_s* s, sv_run_stats* st, std::string& err) {
             }
         }
     }
-    // map: logical at physical nl-g+j <-> logical at physical nl+j
-    for (int j = 0; j < g; ++j) {
-        const int a = s->nl - g + j, b = s->nl + j;
-        for (int& p : s->phys) {
-            if (p == a) p = b;
-            else if (p == b) p = a;
-        }
-    }
+    // (the qubit map update -- physical nl-g+j <-> nl+j -- is done by the planner)
     if (st) {
         st->swaps++;
         st->nvlink_bytes += (uint64_t)chunk * (P - 1);
@@ -179,19 +195,74 @@ uint64_t gate_mask(const Gate& g) {
 
 sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
     std::string err;
-    const auto& gates = p->circ.gates;
-    std::vector<int> pending(gates.size());
-    for (size_t i = 0; i < gates.size(); ++i) pending[i] = (int)i;
     RunOpts o = p->opts;
     if (o.force_kernel == SV_KERNEL_DENSE) o.force_kernel = SV_KERNEL_PER_GATE;  // dense-k needs local targets
-    const int S = nshards(s);
+    std::vector<int> ranks;
+    for (int i = 0; i < nshards(s); ++i) ranks.push_back(rank_of(s, i));
+    // plan cache: the schedule depends only on the map at entry, the shard ranks and dtype
+    ShardPlan* sp = nullptr;
+    for (auto& c : p->shard_cache)
+        if (c.world == s->world && c.dbl == s->dbl && c.ranks == ranks && c.start_phys == s->phys) sp = &c;
+    if (!sp) {
+        ShardPlan plan;
+        const sv_status r = shard_plan(p->circ, o, s->n, s->nl, s->world, s->dbl, ranks, s->phys, plan, err);
+        if (r != SV_OK) return set_err(r, err);
+        p->shard_cache.push_back(std::move(plan));
+        sp = &p->shard_cache.back();
+    }
+    for (ShardStep& step : sp->steps) {
+        sv_status r;
+        if (step.exchange) {
+            r = exchange_all(s, stats, err);
+        } else {
+            for (size_t i = 0; i < step.sched.size(); ++i) {
+                if (o.use_jit()) {
+                    r = jit_prepare(step.sched[i], err);
+                    if (r != SV_OK) return set_err(r, err);
+                }
+                r = run_sched(s, (int)i, step.sched[i], stats, err);
+                if (r != SV_OK) return set_err(r, err);
+            }
+            r = SV_OK;
+        }
+        if (r != SV_OK) return set_err(r, err);
+    }
+    s->phys = sp->end_phys;
+    if (stats) stats->gates = p->circ.gates.size();
+    return SV_OK;
+}
+
+// Host-only planning of a sharded run; see the file header.
+sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int world, bool dbl,
+                     const std::vector<int>& ranks, std::vector<int> phys, ShardPlan& out, std::string& err) {
+    const auto& gates = circ.gates;
+    int g = 0;
+    while ((1 << g) < world) ++g;
+    out = ShardPlan();
+    out.world = world;
+    out.dbl = dbl;
+    out.ranks = ranks;
+    out.start_phys = phys;
+    std::vector<int> pending(gates.size());
+    for (size_t i = 0; i < gates.size(); ++i) pending[i] = (int)i;
+    const int S = (int)ranks.size();
+    auto ctx_for = [&](int rank) {
+        Context c;
+        c.n = n;
+        c.nl = nl;
+        c.world = world;
+        c.rank = rank;
+        c.phys = phys;
+        c.dbl = dbl;
+        return c;
+    };
     while (!pending.empty()) {
         std::vector<std::vector<LOp>> ops(S);
         std::vector<int> deferred;
         uint64_t blocked = 0;
         for (int gi : pending) {
-            const Gate& g = gates[gi];
-            const uint64_t T = gate_mask(g);
+            const Gate& gt = gates[gi];
+            const uint64_t T = gate_mask(gt);
             if (T & blocked) {
                 deferred.push_back(gi);
                 blocked |= T;
@@ -199,9 +270,8 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
             }
             bool needs = false;
             for (int i = 0; i < S; ++i) {
-                const Context ctx = make_ctx(s, rank_of(s, i));
-                const sv_status r = lower_gate(g, gi, ctx, o, ops[i], needs, err);
-                if (r != SV_OK) return set_err(r, err);
+                const sv_status r = lower_gate(gt, gi, ctx_for(ranks[i]), o, ops[i], needs, err);
+                if (r != SV_OK) return r;
                 if (needs) break;
             }
             if (needs) {
@@ -211,61 +281,72 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
         }
         if (!deferred.empty()) {
             // relabel: put the g local logical qubits with the farthest next use at the top
-            const int g = s->g, nl = s->nl;
-            std::vector<long> next_use(s->n, (long)1 << 40);
+            std::vector<long> next_use(n, (long)1 << 40);
             for (size_t i = deferred.size(); i-- > 0;) {
                 const Gate& gg = gates[deferred[i]];
                 for (int q : gg.targets) next_use[q] = (long)i;
                 for (int q : gg.controls) next_use[q] = (long)i;
             }
             std::vector<int> local_logical;
-            for (int q = 0; q < s->n; ++q)
-                if (s->phys[q] < nl) local_logical.push_back(q);
+            for (int q = 0; q < n; ++q)
+                if (phys[q] < nl) local_logical.push_back(q);
             std::stable_sort(local_logical.begin(), local_logical.end(), [&](int a, int b) {
                 if (next_use[a] != next_use[b]) return next_use[a] > next_use[b];
-                return s->phys[a] > s->phys[b];  // prefer qubits already high
+                return phys[a] > phys[b];  // prefer qubits already high
             });
             std::vector<int> F(local_logical.begin(), local_logical.begin() + g);
-            std::vector<int> inF(s->n, 0);
+            std::vector<int> inF(n, 0);
             for (int q : F) inF[q] = 1;
-            std::vector<int> logical_at(s->n);
-            for (int q = 0; q < s->n; ++q) logical_at[s->phys[q]] = q;
+            std::vector<int> logical_at(n);
+            for (int q = 0; q < n; ++q) logical_at[phys[q]] = q;
             for (int q : F) {
-                if (s->phys[q] >= nl - g) continue;
+                if (phys[q] >= nl - g) continue;
                 // a top-local slot whose occupant is not in F
                 for (int t = nl - g; t < nl; ++t) {
                     const int occ = logical_at[t];
                     if (inF[occ]) continue;
-                    const int pq = s->phys[q];
+                    const int pq = phys[q];
                     for (int i = 0; i < S; ++i) ops[i].push_back(phys_swap(pq, t));
-                    std::swap(s->phys[q], s->phys[occ]);
+                    std::swap(phys[q], phys[occ]);
                     logical_at[t] = q;
                     logical_at[pq] = occ;
                     break;
                 }
             }
         }
-        sv_status r = run_ops(s, ops, o, stats, err);
-        if (r != SV_OK) return set_err(r, err);
+        ShardStep batch;
+        for (int i = 0; i < S; ++i) {
+            Schedule sc;
+            const sv_status r = build_schedule(ops[i], ctx_for(ranks[i]), o, sc, err);
+            if (r != SV_OK) return r;
+            batch.sched.push_back(std::move(sc));
+        }
+        out.steps.push_back(std::move(batch));
         if (deferred.empty()) break;
-        r = exchange_all(s, stats, err);
-        if (r != SV_OK) return set_err(r, err);
+        // exchange: logical at physical nl-g+j <-> logical at physical nl+j
+        for (int j = 0; j < g; ++j) {
+            const int a = nl - g + j, b = nl + j;
+            for (int& p : phys) {
+                if (p == a) p = b;
+                else if (p == b) p = a;
+            }
+        }
+        ShardStep ex;
+        ex.exchange = true;
+        out.steps.push_back(std::move(ex));
+        ++out.swaps;
         if (deferred.size() == pending.size()) {
             // the exchange must make the first deferred gate runnable; guard against livelock
             const Gate& g0 = gates[deferred[0]];
             for (int q : g0.targets)
-                if (s->phys[q] >= s->nl && g0.U.size() > 1) {
-                    bool diag = true;
-                    const size_t d = (size_t)1 << g0.targets.size();
-                    for (size_t a = 0; a < d && diag; ++a)
-                        for (size_t b = 0; b < d; ++b)
-                            if (a != b && g0.U[a * d + b] != cd(0, 0)) { diag = false; break; }
-                    if (!diag) return set_err(SV_ERR_STATE, "sharded planner made no progress");
+                if (phys[q] >= nl) {
+                    err = "sharded planner made no progress";
+                    return SV_ERR_STATE;
                 }
         }
         pending = std::move(deferred);
     }
-    if (stats) stats->gates = gates.size();
+    out.end_phys = phys;
     return SV_OK;
 }
 

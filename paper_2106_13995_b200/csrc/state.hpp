@@ -1,5 +1,6 @@
 // state.hpp -- the sv_state / sv_plan objects behind the C-ABI handles.
 #pragma once
+#include <list>
 #include <map>
 #include <string>
 #include <vector>
@@ -38,7 +39,26 @@ struct sv_state_s {
     }
 };
 
+// Host plan of a sharded run: batches of passes per shard, separated by exchange steps.
+struct ShardStep {
+    bool exchange = false;              // swap the g global bits with the g top local bits
+    std::vector<svb::Schedule> sched;   // batch: one schedule per shard run by this process
+};
+
+struct ShardPlan {
+    int world = 0;
+    bool dbl = false;
+    std::vector<int> ranks;             // ranks whose shards this process runs
+    std::vector<int> start_phys, end_phys;
+    std::vector<ShardStep> steps;
+    uint64_t swaps = 0;
+};
+
+sv_status shard_plan(const svb::Circuit& circ, const svb::RunOpts& o, int n, int nl, int world, bool dbl,
+                     const std::vector<int>& ranks, std::vector<int> phys, ShardPlan& out, std::string& err);
+
 struct sv_plan_s {
+    std::list<ShardPlan> shard_cache;   // sharded schedules by (world, ranks, map at entry)
     svb::Circuit circ;
     sv_dtype dtype = SV_C64;
     svb::RunOpts opts;

@@ -56,6 +56,12 @@ class Plan:
         check(lib.sv_plan_info(self._h, ctypes.byref(n), ctypes.byref(g), ctypes.byref(p), ctypes.byref(s)))
         return {"n": n.value, "gates": g.value, "passes": p.value, "stages": s.value}
 
+    def shard_info(self, world: int) -> dict:
+        """Host-only dry run of the sharded schedule over `world` GPUs (no GPU needed)."""
+        s, b, p = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.sv_plan_shard_info(self._h, int(world), ctypes.byref(s), ctypes.byref(b), ctypes.byref(p)))
+        return {"swaps": s.value, "batches": b.value, "passes": p.value}
+
     def pass_times(self):
         """Per-pass device ms of the last apply (plan compiled with profile=True)."""
         n = ctypes.c_int()
@@ -124,17 +130,14 @@ class StateVector:
     @classmethod
     def sharded(cls, n: int, dtype="c64", group=None, stream=None) -> "StateVector":
         """Collective: one process per GPU; torch.distributed broadcasts the NCCL unique id."""
-        import torch
         import torch.distributed as dist
+
+        from .dist import broadcast_unique_id
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         uid = (ctypes.c_uint8 * 128)()
         if rank == 0:
             check(lib.sv_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p)))
-        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
-        if dist.get_backend(group) == "nccl":
-            t = t.cuda()
-        dist.broadcast(t, src=0, group=group)
-        raw = bytes(t.cpu().tolist())
+        raw = broadcast_unique_id(bytes(uid), group)
         ctypes.memmove(uid, raw, 128)
         h = ctypes.c_void_p()
         check(lib.sv_create_sharded(int(n), _dtype(dtype), ctypes.cast(uid, ctypes.c_void_p), world, rank,
