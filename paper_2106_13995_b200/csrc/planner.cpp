@@ -577,26 +577,76 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                 for (int i : todo) leftover.push_back(pass_ops[i]);
                 break;
             }
-            StagePlan sp;
-            uint64_t sblocked = 0;
-            std::vector<int> sdef;
-            for (int i : todo) {
-                const LOp& op = ops[pass_ops[i]];
-                if (op.touched & sblocked) { sdef.push_back(i); sblocked |= op.touched; continue; }
-                const bool wide = (op.kind == OP_U3 || op.kind == OP_U4);
-                if (wide && !sp.wide.empty() && sp.wide != op.tq) { sdef.push_back(i); sblocked |= op.touched; continue; }
-                if (wide && sp.wide.empty()) {
-                    // wide targets go to positions 0..k-1; they must not collide with narrow ops' needs
-                    if (popc(sp.R | qmask(op.tq)) > rb) { sdef.push_back(i); sblocked |= op.touched; continue; }
+            // One stage with register set fixed to `allowed` (0 = grow greedily): ops run in
+            // order; an op that cannot run blocks its qubits for every later op (R21).
+            auto fill_stage = [&](uint64_t allowed, StagePlan& sp, std::vector<int>& sdef, double& score) {
+                uint64_t sblocked = 0;
+                score = 0;
+                for (int i : todo) {
+                    const LOp& op = ops[pass_ops[i]];
+                    if (op.touched & sblocked) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                    const bool wide = (op.kind == OP_U3 || op.kind == OP_U4);
+                    if (wide && !sp.wide.empty() && sp.wide != op.tq) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                    const uint64_t need = sp.R | qmask(op.tq);
+                    const bool fits = allowed ? ((qmask(op.tq) & ~allowed) == 0) : popc(need) <= rb;
+                    if (fits) {
+                        sp.R = need;
+                        sp.ops.push_back(i);
+                        score += op_cost(op);
+                        if (wide) sp.wide = op.tq;
+                    } else {
+                        sdef.push_back(i);
+                        sblocked |= op.touched;
+                    }
                 }
-                const uint64_t need = sp.R | qmask(op.tq);
-                if (popc(need) <= rb) {
-                    sp.R = need;
-                    sp.ops.push_back(i);
-                    if (wide) sp.wide = op.tq;
-                } else {
-                    sdef.push_back(i);
-                    sblocked |= op.touched;
+            };
+            StagePlan sp;
+            std::vector<int> sdef;
+            double best_score;
+            fill_stage(0, sp, sdef, best_score);
+            // Search: the register set that lets this stage run the most work (targets of the
+            // next non-diagonal ops, all rb-subsets when there are few enough).  Fewer stages
+            // means fewer shared-memory transitions.  The first stage avoids the lowest qubits
+            // (they would cost an extra coalescing stage).
+            {
+                uint64_t Q = 0;
+                int seen = 0;
+                for (int i : todo) {
+                    const LOp& op = ops[pass_ops[i]];
+                    if (op.tq.empty()) continue;
+                    Q |= qmask(op.tq);
+                    if (++seen >= 24) break;
+                }
+                std::vector<int> qs;
+                for (int q = 0; q < 64; ++q)
+                    if ((Q >> q) & 1) qs.push_back(q);
+                const int cl = dbl ? 2 : 3;
+                const uint64_t lowq = (1ull << cl) - 1;
+                auto penalty = [&](uint64_t R) { return (stages.empty() && (R & lowq)) ? 3.0 : 0.0; };
+                double best = best_score - penalty(sp.R);
+                const int nq = (int)qs.size();
+                if (nq > rb && nq <= 16) {
+                    // enumerate rb-subsets of qs (Gosper's hack)
+                    uint32_t c = (1u << rb) - 1;
+                    int evaluated = 0;
+                    while (c < (1u << nq) && evaluated < 5000) {
+                        uint64_t R = 0;
+                        for (int j = 0; j < nq; ++j)
+                            if ((c >> j) & 1) R |= 1ull << qs[j];
+                        StagePlan sp2;
+                        std::vector<int> sdef2;
+                        double sc2;
+                        fill_stage(R, sp2, sdef2, sc2);
+                        const double v = sc2 - penalty(sp2.R);
+                        if (v > best + 1e-9) {
+                            best = v;
+                            sp = std::move(sp2);
+                            sdef = std::move(sdef2);
+                        }
+                        ++evaluated;
+                        const uint32_t u = c & (0u - c), w = c + u;
+                        c = w | (((w ^ c) >> 2) / u);
+                    }
                 }
             }
             if (diag_into_regs()) {
