@@ -463,6 +463,30 @@ bool write_tile_params(const TileSym& sym, const Context& ctx, PassPlan& pp, std
 
 size_t coef_size(const LOp& op) { return op.coef.size(); }
 
+// Commutation-aware blocking (reading R21): an op's qubits split into non-diagonal targets T
+// and diagonal qubits / controls D.  Two ops commute when T(A) avoids T(B) and D(B) and T(B)
+// avoids D(A) -- both are block-diagonal in the D qubits, which neither changes -- so a later
+// op only waits for an earlier deferred op when that condition fails.
+struct Blocker {
+    uint64_t T = 0, D = 0;
+    static uint64_t dmask(const LOp& op) { return qmask(op.dq) | qmask(op.ctrl); }
+    bool blocks(const LOp& op) const {
+        if (!commute_rule()) return (qmask(op.tq) | dmask(op)) & (T | D);
+        return (qmask(op.tq) & (T | D)) || (dmask(op) & T);
+    }
+    void add(const LOp& op) {
+        T |= qmask(op.tq);
+        D |= dmask(op);
+    }
+    static bool commute_rule() {
+        static const bool b = [] {
+            const char* e = getenv("SV_COMMUTE");
+            return e ? atoi(e) != 0 : true;
+        }();
+        return b;
+    }
+};
+
 // Estimated issue cost of an op in the generated kernel, in instructions per amplitude
 // (calibrated on the SASS of generated passes, tools/sass_stats.py).  A pass stays
 // HBM-bound while its total stays below the budget: one pass moves 2 x 2^n x b bytes in
@@ -495,7 +519,9 @@ bool diag_into_regs() {
 double pass_budget() {
     static double b = [] {
         const char* e = getenv("SV_PASS_BUDGET");
-        return e ? atof(e) : 110.0;
+        // measured (tools/sweep_planner.sh, profiles/r01_planner_sweep.txt): with the generated
+        // kernels fewer, fuller passes win; the cap stays as a knob, off by default
+        return e ? atof(e) : 1000.0;
     }();
     return b;
 }
@@ -535,7 +561,8 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
     while (!remaining.empty()) {
         // ---- choose the pass's gates and tile qubits
         std::vector<int> pass_ops, deferred;
-        uint64_t S = lowmask, blocked = 0;
+        uint64_t S = lowmask;
+        Blocker blocked;
         size_t ncoef = 0;
         double cost = 0;
         const double budget = o.use_jit() ? pass_budget() : 1e30;
@@ -551,9 +578,9 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                                        : (pass_ops.size() >= (size_t)kMaxOps ||
                                           ncoef + coef_size(op) > (size_t)kMaxCoefComplex ||
                                           (!pass_ops.empty() && cost + op_cost(op) > budget));
-            if (op.densek || full || (op.touched & blocked)) {
+            if (op.densek || full || blocked.blocks(op)) {
                 deferred.push_back(idx);
-                blocked |= op.touched;
+                blocked.add(op);
                 continue;
             }
             const uint64_t need = S | qmask(op.tq);
@@ -564,7 +591,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                 cost += op_cost(op);
             } else {
                 deferred.push_back(idx);
-                blocked |= op.touched;
+                blocked.add(op);
             }
         }
         // ---- cut the pass into register stages
@@ -580,13 +607,13 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
             // One stage with register set fixed to `allowed` (0 = grow greedily): ops run in
             // order; an op that cannot run blocks its qubits for every later op (R21).
             auto fill_stage = [&](uint64_t allowed, StagePlan& sp, std::vector<int>& sdef, double& score) {
-                uint64_t sblocked = 0;
+                Blocker sblocked;
                 score = 0;
                 for (int i : todo) {
                     const LOp& op = ops[pass_ops[i]];
-                    if (op.touched & sblocked) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                    if (sblocked.blocks(op)) { sdef.push_back(i); sblocked.add(op); continue; }
                     const bool wide = (op.kind == OP_U3 || op.kind == OP_U4);
-                    if (wide && !sp.wide.empty() && sp.wide != op.tq) { sdef.push_back(i); sblocked |= op.touched; continue; }
+                    if (wide && !sp.wide.empty() && sp.wide != op.tq) { sdef.push_back(i); sblocked.add(op); continue; }
                     const uint64_t need = sp.R | qmask(op.tq);
                     const bool fits = allowed ? ((qmask(op.tq) & ~allowed) == 0) : popc(need) <= rb;
                     if (fits) {
@@ -596,7 +623,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                         if (wide) sp.wide = op.tq;
                     } else {
                         sdef.push_back(i);
-                        sblocked |= op.touched;
+                        sblocked.add(op);
                     }
                 }
             };
