@@ -107,3 +107,47 @@ def test_random_state_normalised():
     psi = W.random_state(10, 0)
     assert abs(np.sum(np.abs(psi) ** 2) - 1) < 1e-12
     assert np.array_equal(psi, W.random_state(10, 0))
+
+
+# ------------------------------------------------------------------ width sweep
+def test_remove_random_qubit_examples():
+    rng = W.circuits.Xoshiro256ss(1)
+    c = W.Circuit(2, [[W.GateSpec("CNOT", (0, 1))]])
+    r = W.remove_random_qubit(c, rng)
+    assert r.n == 1 and W.gate_count(r) == 0 and r.depth == 0
+    c = W.Circuit(3, [[W.GateSpec("H", (0,)), W.GateSpec("H", (1,)), W.GateSpec("H", (2,))]])
+    for seed in range(20):
+        r = W.remove_random_qubit(c, W.circuits.Xoshiro256ss(seed))
+        assert r.n == 2 and [g.qubits for g in r.gates] == [(0,), (1,)]
+    big = W.supremacy(5, 4, 8, seed=0)
+    r = W.remove_random_qubit(big, W.circuits.Xoshiro256ss(3))
+    assert r.n == 19 and W.gate_count(r) < W.gate_count(big)
+
+
+def test_width_sweep_properties():
+    base = W.multiplier(3)  # 13 qubits
+    sweep = W.width_sweep(base, 9, seed=5)
+    assert [c.n for c in sweep] == [12, 11, 10, 9]
+    prev = base
+    for c in sweep:
+        # nested gate sets under the recorded renumbering
+        r = c.meta["removed"][-1]
+        back = lambda q: q if q < r else q + 1  # noqa: E731
+        prev_set = {(g.name, g.qubits) for g in prev.gates}
+        assert all((g.name, tuple(back(q) for q in g.qubits)) in prev_set for g in c.gates)
+        for g in c.gates:
+            assert max(g.all_qubits()) < c.n
+        prev = c
+    assert [W.to_text(c) for c in sweep] == [W.to_text(c) for c in W.width_sweep(base, 9, seed=5)]
+    with pytest.raises(ValueError):
+        W.width_sweep(base, 13, seed=0)
+    assert len(W.width_sweep(W.supremacy(5, 1, 2), 4, seed=0)) == 1
+
+
+def test_family_at_width():
+    for n in (13, 19, 25, 28):
+        assert W.family_at_width("supremacy", n).n == n
+    for n in (13, 14, 16, 17, 21):
+        c = W.family_at_width("multiplier", n)
+        assert c.n == n
+    assert W.gate_count(W.family_at_width("multiplier", 17)) == W.gate_count(W.multiplier(4))

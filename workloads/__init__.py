@@ -25,5 +25,8 @@ from .circuits import (  # noqa: F401
     basis_prep,
     to_text,
     gate_count,
+    remove_random_qubit,
+    width_sweep,
+    family_at_width,
 )
 from .states import random_state, round_to_c64  # noqa: F401

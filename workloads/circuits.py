@@ -305,6 +305,68 @@ def concat(a: Circuit, b: Circuit) -> Circuit:
                    a.family + "+" + b.family, dict(a.meta))
 
 
+# ---------------------------------------------------------------- width sweep (f3)
+def remove_random_qubit(c: Circuit, rng: Xoshiro256ss) -> Circuit:
+    """SPEC S:281-289 / P:63: pick a qubit uniformly, delete every gate that touches it,
+    renumber the remaining qubits in order, drop empty moments, record the removed index."""
+    if c.n < 2:
+        raise ValueError("cannot remove a qubit from a 1-qubit circuit")
+    r = rng.below(c.n)
+
+    def remap(q):
+        return q if q < r else q - 1
+
+    moments = []
+    for m in c.moments:
+        kept = []
+        for g in m:
+            if r in g.all_qubits():
+                continue
+            kept.append(GateSpec(g.name, tuple(remap(q) for q in g.qubits), tuple(remap(q) for q in g.controls),
+                                 g.matrix))
+        if kept:
+            moments.append(kept)
+    removed = list(c.meta.get("removed", [])) + [r]
+    return Circuit(c.n - 1, moments, c.family, dict(c.meta, removed=removed))
+
+
+def width_sweep(base: Circuit, min_width: int, seed: int) -> List[Circuit]:
+    """SPEC S:291-299 / P:63: circuits of widths base.n-1 down to min_width, each obtained
+    from the previous one by one random qubit removal (deterministic for a seed)."""
+    if min_width >= base.n:
+        raise ValueError("min_width must be below the base width")
+    rng = Xoshiro256ss(seed)
+    out, cur = [], base
+    while cur.n > min_width:
+        cur = remove_random_qubit(cur, rng)
+        out.append(cur)
+    return out
+
+
+def family_at_width(family: str, n: int, seed: int = 0, depth: int = 20) -> Circuit:
+    """The paper's method for non-standard widths: build the next larger standard circuit
+    and remove random qubits.  Supremacy: square-ish grids (rows x cols, rows >= cols); multiplier:
+    width 4k+1."""
+    if family == "supremacy":
+        best = None
+        for cols in range(2, 12):
+            for rows in range(cols, 24):
+                if rows * cols >= n and (best is None or rows * cols < best[0] * best[1]):
+                    best = (rows, cols)
+        rows, cols = best
+        c = supremacy(rows, cols, depth, seed)
+    elif family == "multiplier":
+        k = 1
+        while 4 * k + 1 < n:
+            k += 1
+        c = multiplier(k)
+    else:
+        raise ValueError(family)
+    if c.n == n:
+        return c
+    return width_sweep(c, n, seed)[-1]
+
+
 # ---------------------------------------------------------------- writer
 def _fmt(x: float) -> str:
     return repr(float(x))
