@@ -205,7 +205,11 @@ sv_status plan_schedule(sv_plan_s* p) {
     if (st != SV_OK) return fail(st, err);
     // a reversible circuit: one gather pass, unless its scattered reads cost more than the
     // fused tile passes (both estimated in HBM passes)
-    if (have_perm && perm.passes[0].perm_cost < 1.2 * (double)p->sched.passes.size()) p->sched = std::move(perm);
+    if (have_perm) {
+        double pc = 0;
+        for (const PassPlan& pp : perm.passes) pc += pp.kind == PassPlan::PERM ? pp.perm_cost : 1.0;
+        if (pc < 1.2 * (double)p->sched.passes.size()) p->sched = std::move(perm);
+    }
     p->cached = true;
     p->jitted = false;
     return SV_OK;
@@ -546,7 +550,8 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
         if (st != SV_OK) return fail(st, err);
         p->jitted = true;
     }
-    sv_status st = SV_OK;
+    sv_status st = canonicalize(s);  // the plan assumes the identity layout
+    if (st != SV_OK) return st;
     if (p->opts.use_graph) {
         if (!p->graph || p->graph_ptr != s->d || p->graph_stream != s->stream) {
             if (p->graph) cudaGraphExecDestroy(p->graph);
@@ -585,6 +590,7 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
         st = run_schedule(s, s->d, p->sched, stats, p->opts.profile ? &p->prof_ev : nullptr);
         p->prof_n = p->opts.profile ? (int)p->sched.passes.size() : 0;
     }
+    if (st == SV_OK && !p->sched.end_phys.empty()) s->phys = p->sched.end_phys;  // layout-changing plan
     if (stats) stats->gates = p->circ.gates.size();
     return st;
 }

@@ -111,6 +111,7 @@ struct PassPlan {
 struct Schedule {
     std::vector<PassPlan> passes;
     uint64_t stages = 0;
+    std::vector<int> end_phys;   // qubit map after the schedule if it changes the layout (else empty)
 };
 
 sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,

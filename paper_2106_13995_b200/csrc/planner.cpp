@@ -77,28 +77,24 @@ bool build_perm_schedule(const Circuit& c, const Context& ctx, const RunOpts& o,
         }
         pp.perm.push_back(pg);
     }
-    for (PermGate& pg : pp.perm) {  // logical -> physical (identity on one GPU)
-        pg.t = ctx.phys[pg.t];
-        if (pg.t2 >= 0) pg.t2 = ctx.phys[pg.t2];
-        for (int& q : pg.ctrl) q = ctx.phys[q];
-    }
     pp.touched_amps = 1ull << ctx.nl;
     pp.m = ctx.nl;  // qubits of the (local) state
     pp.perm_dbl = ctx.dbl;
+    const int n = ctx.nl;
     // Cost model (HBM passes): the gather is coalesced only where f^-1 keeps a warp's 32
     // sources together.  Sample warps on the host, count distinct 32-byte sectors per gather.
-    {
+    auto cost_of = [&](const std::vector<PermGate>& gates) {
         uint64_t seed = 0x9E3779B97F4A7C15ull, sectors = 0, gathers = 0;
         const int ab = ctx.dbl ? 16 : 8;
         for (int w = 0; w < 64; ++w) {
             seed = seed * 6364136223846793005ull + 1442695040888963407ull;
-            const uint64_t base = ((seed >> 11) << 10) & ((1ull << ctx.nl) - 1) & ~1023ull;
+            const uint64_t base = ((seed >> 11) << 10) & ((1ull << n) - 1) & ~1023ull;
             for (int s = 0; s < 32; s += 7) {
                 std::vector<uint64_t> sec;
                 for (int lane = 0; lane < 32; ++lane) {
                     uint64_t x = base | (uint64_t)lane | ((uint64_t)s << 5);
-                    for (size_t i = pp.perm.size(); i-- > 0;) {
-                        const PermGate& g = pp.perm[i];
+                    for (size_t i = gates.size(); i-- > 0;) {
+                        const PermGate& g = gates[i];
                         bool on = true;
                         for (int c : g.ctrl) on &= ((x >> c) & 1) != 0;
                         if (!on) continue;
@@ -116,10 +112,57 @@ bool build_perm_schedule(const Circuit& c, const Context& ctx, const RunOpts& o,
         const double ratio = (double)sectors / gathers / ideal;
         // measured on B200: 32 distinct sectors per 8-byte gather (ratio 4) read 12x the bytes
         const double read_factor = ratio <= 1.25 ? 1.0 : std::min(12.0, 3.0 * ratio);
-        pp.perm_cost = 0.5 * (read_factor + 1.0);
+        return 0.5 * (read_factor + 1.0);
+    };
+    // Layout choice: the gather coalesces when the warp's lanes sit on qubits that f^-1 only
+    // shifts among themselves (for a multiplier: the low bits of the product register, not the
+    // operand).  Candidates swap a window of 5 logical qubits into the 5 lowest physical
+    // positions; a relabel pass (SWAP ops in one tile pass) costs ~1 HBM pass and leaves the
+    // state in that layout (the qubit map records it; readout canonicalises).
+    const std::vector<PermGate> logical = pp.perm;
+    auto mapped = [&](const std::vector<int>& phys) {
+        std::vector<PermGate> g = logical;
+        for (PermGate& pg : g) {
+            pg.t = phys[pg.t];
+            if (pg.t2 >= 0) pg.t2 = phys[pg.t2];
+            for (int& q : pg.ctrl) q = phys[q];
+        }
+        return g;
+    };
+    std::vector<int> best_phys = ctx.phys;
+    double best = cost_of(mapped(best_phys));
+    for (int k = 5; k + 5 <= n && best > 1.0; ++k) {
+        std::vector<int> phys = ctx.phys;
+        for (int i = 0; i < 5; ++i) std::swap(phys[i], phys[k + i]);
+        const double c2 = 1.0 + cost_of(mapped(phys));
+        if (c2 < best) {
+            best = c2;
+            best_phys = phys;
+        }
     }
+    if (best_phys != ctx.phys) {
+        std::vector<LOp> sw;
+        for (int i = 0; i < 5; ++i) {
+            // physical swap of the positions of logical i and the window qubit now at i
+            int k = -1;
+            for (int q = 0; q < n; ++q)
+                if (best_phys[q] == ctx.phys[i]) k = q;
+            const int a = ctx.phys[i], b = ctx.phys[k];
+            if (a == b) continue;
+            LOp op;
+            op.kind = OP_SWAP;
+            op.tq = {std::min(a, b), std::max(a, b)};
+            op.touched = qmask(op.tq);
+            sw.push_back(op);
+        }
+        std::string err;
+        if (build_schedule(sw, ctx, o, out, err) != SV_OK) return false;
+    }
+    pp.perm = mapped(best_phys);
+    pp.perm_cost = best;
     pp.nops = (int)pp.perm.size();
     out.passes.push_back(std::move(pp));
+    out.end_phys = best_phys;
     return true;
 }
 

@@ -353,7 +353,9 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
 // Bring the qubit map back to the identity: single-bit exchanges for the global positions,
 // then a batch of physical SWAP ops for the local positions.
 sv_status sharded_canonicalize(sv_state_s* s) {
-    if (s->world == 1) return SV_OK;
+    bool identity = true;
+    for (int q = 0; q < s->n; ++q) identity &= s->phys[q] == q;
+    if (identity) return SV_OK;  // single GPU: only relabelled by layout-changing plans
     std::string err;
     RunOpts o;
     const int nl = s->nl, g = s->g;
