@@ -83,6 +83,9 @@ struct TileSym {                 // symbolic tile pass: what both backends execu
     int rb = 0;
     bool dbl = false;
     std::vector<StageSym> stages;
+    // optional relabel on store (generated kernels only): physical qubit q of the input is
+    // written at physical position out_perm[q]; a permutation of the tile qubits
+    std::vector<int> out_perm;
 };
 
 // A classical reversible gate for the whole-permutation pass: X on t (or SWAP of t, t2)

@@ -583,6 +583,23 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
                 o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
             }
             o << "\n";
+            if (!sym.out_perm.empty()) {
+                // relabel on store: thread bits and register bits go to their output positions
+                std::vector<int> outpos;
+                for (int q : tq_phys) outpos.push_back(sym.out_perm[q]);
+                // deposit_expr needs ascending thread-bit order only for run detection; build a
+                // plain OR of single bits instead
+                std::string ex;
+                for (size_t i = 0; i < outpos.size(); ++i)
+                    ex += "|((unsigned long long)((t>>" + std::to_string(i) + ")&1u)<<" + std::to_string(outpos[i]) + ")";
+                o << "g=base" << ex << ";\n";
+                for (int s = 0; s < R; ++s) {
+                    uint64_t go = 0;
+                    for (int j = 0; j < rb; ++j)
+                        if ((s >> j) & 1) go |= 1ull << sym.out_perm[st.rq[j]];
+                    goff[s] = go;
+                }
+            }
             for (int s = 0; s < R; ++s) o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
             o << "\n";
         } else {

@@ -55,6 +55,11 @@ uint64_t qmask(const std::vector<int>& qs) {
 
 int default_rb(bool dbl, int nl) { return std::max(1, std::min(dbl ? 4 : 5, nl)); }
 
+namespace {
+template <typename real>
+bool write_tile_params(const TileSym& sym, const Context& ctx, PassPlan& pp, std::string& err);
+}
+
 bool build_perm_schedule(const Circuit& c, const Context& ctx, const RunOpts& o, Schedule& out) {
     if (!o.use_jit() || ctx.world != 1 || ctx.nl < 10 || ctx.nl > 32 || c.gates.empty()) return false;
     static const bool enabled = [] {
@@ -141,22 +146,36 @@ bool build_perm_schedule(const Circuit& c, const Context& ctx, const RunOpts& o,
         }
     }
     if (best_phys != ctx.phys) {
-        std::vector<LOp> sw;
-        for (int i = 0; i < 5; ++i) {
-            // physical swap of the positions of logical i and the window qubit now at i
-            int k = -1;
-            for (int q = 0; q < n; ++q)
-                if (best_phys[q] == ctx.phys[i]) k = q;
-            const int a = ctx.phys[i], b = ctx.phys[k];
-            if (a == b) continue;
-            LOp op;
-            op.kind = OP_SWAP;
-            op.tq = {std::min(a, b), std::max(a, b)};
-            op.touched = qmask(op.tq);
-            sw.push_back(op);
-        }
+        // The relabel pass: no ops, one shared-memory transition; it loads with the low qubits
+        // as lanes and stores with the window qubits as lanes, at their new positions.
+        int k = -1;
+        for (int q = 5; q < n; ++q)
+            if (best_phys[q] == ctx.phys[0]) k = q;  // logical k now sits at physical 0
+        const int rb = default_rb(ctx.dbl, n);
+        const int m = std::min(rb + 8, n);
+        uint64_t S = 0x1Full;
+        for (int i = 0; i < 5; ++i) S |= 1ull << (k + i);
+        for (int q = k + 5; q < n && popc(S) < m; ++q) S |= 1ull << q;   // padding above the window
+        for (int q = 5; q < n && popc(S) < m; ++q) S |= 1ull << q;       // (or below if needed)
+        PassPlan rp;
+        rp.sym = std::make_shared<TileSym>();
+        TileSym& sym = *rp.sym;
+        for (int q = 0; q < 64; ++q)
+            if ((S >> q) & 1) sym.tq.push_back(q);
+        sym.rb = rb;
+        sym.dbl = ctx.dbl;
+        StageSym s0, s1;
+        for (int b = (int)sym.tq.size() - 1; b >= 0 && (int)s0.rq.size() < rb; --b) s0.rq.push_back(sym.tq[b]);
+        for (int q = 0; q < rb; ++q) s1.rq.push_back(q);
+        sym.stages = {s0, s1};
+        sym.out_perm.resize(64);
+        for (int q = 0; q < 64; ++q) sym.out_perm[q] = q;
+        for (int i = 0; i < 5; ++i) std::swap(sym.out_perm[i], sym.out_perm[k + i]);
         std::string err;
-        if (build_schedule(sw, ctx, o, out, err) != SV_OK) return false;
+        const bool ok = ctx.dbl ? write_tile_params<double>(sym, ctx, rp, err) : write_tile_params<float>(sym, ctx, rp, err);
+        if (!ok) return false;
+        out.stages += 2;
+        out.passes.push_back(std::move(rp));
     }
     pp.perm = mapped(best_phys);
     pp.perm_cost = best;
