@@ -668,6 +668,17 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
         if (p < s->nl) { lq.push_back(p); lj.push_back(j); }
         else { gq.push_back(p); gj.push_back(j); }
     }
+    {
+        // kernel bins in physical bit order (neighbouring bins = neighbouring amplitudes);
+        // the host remap below puts them in the caller's order
+        std::vector<int> idx(lq.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+        std::sort(idx.begin(), idx.end(), [&](int a, int b) { return lq[a] < lq[b]; });
+        std::vector<int> lq2, lj2;
+        for (int i : idx) { lq2.push_back(lq[i]); lj2.push_back(lj[i]); }
+        lq = lq2;
+        lj = lj2;
+    }
     const int nql = (int)lq.size();
     MarginalParams P{};
     P.nq = nql;
