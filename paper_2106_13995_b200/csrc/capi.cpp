@@ -477,7 +477,8 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     std::string src;
     int threads;
     size_t smem;
-    if (pp.kind == PassPlan::TILE && pp.sym) src = gen_pass_source(*pp.sym, threads, smem);
+    bool pers;
+    if (pp.kind == PassPlan::TILE && pp.sym) src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers);
     else if (pp.kind == PassPlan::PERM) src = gen_perm_source(pp, pp.perm_dbl, threads);
     if (len) *len = src.size();
     if (buf && cap) {

@@ -104,6 +104,8 @@ struct PassPlan {
     void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
     int jit_threads = 0;
     size_t jit_smem = 0;
+    bool jit_persistent = false;         // TILE: persistent grid (prefetching kernel)
+    unsigned jit_grid = 0;
     int rb = 0, m = 0, nstages = 0;
     uint64_t ntiles = 0, groups = 0;
     int nops = 0;

@@ -458,7 +458,26 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
     if (cm) e.o << "}\n";
 }
 
-uint32_t swz_const(uint32_t x, bool dbl) { return swizzle_slot(x, dbl ? 3 : 4); }
+// Shared-memory slot swizzle (GF(2)-linear, see sv_kernels.hpp).  With cp.async prefetch
+// (16-byte chunks) a complex64 slot pair must stay adjacent: the XOR then spares bit 0.
+uint32_t swz_mask(bool dbl, bool pf) { return dbl ? 7u : (pf ? 0xEu : 0xFu); }
+uint32_t swz_const(uint32_t x, bool dbl, bool pf) {
+    const int lb = dbl ? 3 : 4;
+    uint32_t y = x >> lb, f = 0;
+    while (y) {
+        f ^= y & ((1u << lb) - 1);
+        y >>= lb;
+    }
+    return x ^ (f & swz_mask(dbl, pf));
+}
+
+bool prefetch_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_PREFETCH");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
 
 // run-length emission of  sum_i ((t >> i) & 1) << dst[i]
 std::string deposit_expr(const std::vector<int>& dst, bool wide) {
@@ -483,7 +502,7 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 
 }  // namespace
 
-std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
+std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent) {
     Em e;
     e.dbl = sym.dbl;
     const int rb = sym.rb, R = 1 << rb;
@@ -491,7 +510,10 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
     const int tb = m - rb;
     threads = 1 << tb;
     const bool multi = sym.stages.size() > 1;
-    smem = multi ? ((size_t)1 << m) * (sym.dbl ? 16 : 8) : 0;
+    const bool pf = prefetch_enabled() && sym.out_perm.empty() && m >= (sym.dbl ? 4 : 5) + 1 &&
+                    ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)threads == 0;
+    persistent = pf;
+    smem = pf ? 2 * ((size_t)1 << m) * (sym.dbl ? 16 : 8) : multi ? ((size_t)1 << m) * (sym.dbl ? 16 : 8) : 0;
     int local_of[64];
     for (int i = 0; i < 64; ++i) local_of[i] = -1;
     for (int b = 0; b < m; ++b) local_of[sym.tq[b]] = b;
@@ -516,21 +538,67 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
              "DI C I(C a){return pk(-hi(a),lo(a));}\n"
              "DI C NI(C a){return pk(hi(a),-lo(a));}\n";
     }
+    // pf: persistent CTAs; the next tile is prefetched into the second shared-memory buffer
+    // with cp.async while this one is computed (HBM reads overlap the arithmetic)
+    const uint32_t smask = swz_mask(sym.dbl, pf);
+    size_t first = 0;
+    if (pf)
+        while (first + 1 < sym.stages.size() && sym.stages[first].ops.empty()) ++first;  // I/O-only stage
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
-      << (threads >= 512 ? 1 : threads >= 256 ? 2 : 4)
-      << ") svpass(C* __restrict__ psi){\n";
-    if (multi) o << "extern __shared__ C sm[];\n";
+      << (pf ? 1 : threads >= 512 ? 1 : threads >= 256 ? 2 : 4) << ") svpass(C* __restrict__ psi){\n";
+    if (multi || pf) o << "extern __shared__ C sm[];\n";
     o << "const unsigned t=threadIdx.x;\n";
-    o << "unsigned long long base=blockIdx.x;\n";
+    o << "C v[" << R << "];\nunsigned long long g,base;\n";
+    if (multi || pf) o << "unsigned tl;\n";
+    const int L = sym.dbl ? 4 : 5;  // the tile's low qubits 0..L-1 are contiguous in memory
+    if (pf) {
+        const int E = sym.dbl ? 1 : 2;  // elements per 16-byte chunk
+        const uint64_t chunks = ((uint64_t)1 << m) / E;
+        const int cpt = (int)(chunks / threads);
+        auto dep = [&](uint64_t x) {  // tile-local element index -> global offset
+            uint64_t r = x & ((1ull << L) - 1);
+            for (int b = L; b < m; ++b)
+                if ((x >> b) & 1) r |= 1ull << sym.tq[b];
+            return r;
+        };
+        o << "C* bc=sm; C* bn=sm+" << (1ull << m) << ";\n";
+        // per-thread part of the chunk addresses (linear in the chunk index)
+        o << "unsigned long long pg=0; unsigned ps=0;\n";
+        o << "{unsigned x=" << E << "u*t;";
+        for (int b = 0; b < tb + (E == 2 ? 1 : 0) && b < m; ++b)
+            o << "if((x>>" << b << ")&1u){pg|=" << dep(1ull << b) << "ull;ps^=" << swz_const(1u << b, sym.dbl, pf)
+              << "u;}";
+        o << "}\n";
+        o << "auto PF=[&](unsigned long long tl_,C* buf){unsigned long long b_=tl_;\n";
+        for (int b = 0; b < m; ++b) {
+            const int q = sym.tq[b];
+            o << "b_=((b_>>" << q << ")<<" << (q + 1) << ")|(b_&" << ((1ull << q) - 1) << "ull);";
+        }
+        o << "\nconst char* src=(const char*)(psi+b_+pg); const unsigned sb=(unsigned)__cvta_generic_to_shared(buf);\n";
+        for (int i = 0; i < cpt; ++i) {
+            const uint64_t xi = (uint64_t)E * threads * i;
+            o << "asm volatile(\"cp.async.cg.shared.global [%0],[%1],16;\"::\"r\"(sb+((ps^" << swz_const((uint32_t)xi, sym.dbl, pf)
+              << "u)<<" << (sym.dbl ? 4 : 3) << ")),\"l\"(src+" << dep(xi) * (sym.dbl ? 16 : 8) << "ull));";
+        }
+        o << "\n};\n";
+        o << "const unsigned long long NT=" << ntiles << "ull;\n";
+        o << "unsigned long long tile=blockIdx.x;\n";
+        o << "PF(tile,bc); asm volatile(\"cp.async.commit_group;\");\n";
+        o << "for(;tile<NT;tile+=gridDim.x){\n";
+        o << "{const unsigned long long nt=tile+gridDim.x; if(nt<NT) PF(nt,bn); asm volatile(\"cp.async.commit_group;\");}\n";
+        o << "asm volatile(\"cp.async.wait_group 1;\"); __syncthreads();\n";
+        o << "base=tile;\n";
+    } else {
+        o << "base=blockIdx.x;\n";
+    }
     for (int b = 0; b < m; ++b) {
         const int q = sym.tq[b];
         o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
     }
-    o << "C v[" << R << "];\nunsigned long long g;\n";
-    if (multi) o << "unsigned tl;\n";
+    const std::string SM = pf ? "bc" : "sm";
     PassState ps;
     ps.ph.assign(R, cd(1, 0));
-    for (size_t si = 0; si < sym.stages.size(); ++si) {
+    for (size_t si = first; si < sym.stages.size(); ++si) {
         const StageSym& st = sym.stages[si];
         StageCtx sc;
         sc.rb = rb;
@@ -551,21 +619,23 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
             for (int j = 0; j < rb; ++j)
                 if ((s >> j) & 1) { go |= 1ull << st.rq[j]; lo |= 1u << local_of[st.rq[j]]; }
             goff[s] = go;
-            loff[s] = swz_const(lo, sym.dbl);
+            loff[s] = swz_const(lo, sym.dbl, pf);
         }
-        if (multi) {
+        const bool reads_smem = pf || si > first;
+        const bool writes_smem = si + 1 < sym.stages.size();
+        if (reads_smem || writes_smem) {
             const std::string tl = deposit_expr(tq_local, false);
             const int lb = sym.dbl ? 3 : 4;
             o << "tl=" << tl << ";\n";
             o << "{unsigned y=tl>>" << lb << ", f=0; while(y){f^=y&" << ((1u << lb) - 1) << "u; y>>=" << lb
-              << ";} tl^=f;}\n";
+              << ";} tl^=f&" << smask << "u;}\n";
         }
-        if (si == 0) {
+        if (!reads_smem) {
             for (int s = 0; s < R; ++s) o << reg(s) << "=psi[g+" << goff[s] << "ull];";
             o << "\n";
         } else {
-            o << "__syncthreads();\n";
-            for (int s = 0; s < R; ++s) o << reg(s) << "=sm[tl^" << loff[s] << "u];";
+            if (si > first) o << "__syncthreads();\n";
+            for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[tl^" << loff[s] << "u];";
             o << "\n";
         }
         for (const LOp& op : st.ops) emit_op(e, op, sc, ps);
@@ -587,8 +657,6 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
                 // relabel on store: thread bits and register bits go to their output positions
                 std::vector<int> outpos;
                 for (int q : tq_phys) outpos.push_back(sym.out_perm[q]);
-                // deposit_expr needs ascending thread-bit order only for run detection; build a
-                // plain OR of single bits instead
                 std::string ex;
                 for (size_t i = 0; i < outpos.size(); ++i)
                     ex += "|((unsigned long long)((t>>" + std::to_string(i) + ")&1u)<<" + std::to_string(outpos[i]) + ")";
@@ -605,10 +673,11 @@ std::string gen_pass_source(const TileSym& sym, int& threads, size_t& smem) {
         } else {
             // unit phases are tied to this stage's register numbering: apply before re-distribution
             for (int s = 0; s < R; ++s) flush_ph(e, ps, s);
-            for (int s = 0; s < R; ++s) o << "sm[tl^" << loff[s] << "u]=" << reg(s) << ";";
+            for (int s = 0; s < R; ++s) o << SM << "[tl^" << loff[s] << "u]=" << reg(s) << ";";
             o << "\n";
         }
     }
+    if (pf) o << "__syncthreads(); {C* tmp=bc; bc=bn; bn=tmp;}\n}\n";
     o << "}\n";
     return o.str();
 }
@@ -757,7 +826,8 @@ sv_status jit_prepare(Schedule& sc, std::string& err) {
             todo[i]->jit_smem = 0;
             todo[i]->ntiles = ((1ull << todo[i]->m) >> 5) / (uint64_t)todo[i]->jit_threads;
         } else {
-            srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->jit_threads, todo[i]->jit_smem);
+            srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->ntiles, todo[i]->jit_threads, todo[i]->jit_smem,
+                                      todo[i]->jit_persistent);
         }
     }
     std::vector<sv_status> st(todo.size(), SV_OK);
@@ -780,14 +850,22 @@ sv_status jit_prepare(Schedule& sc, std::string& err) {
             return st[i];
         }
         todo[i]->jit_fn = fns[i];
+        if (todo[i]->jit_persistent) {
+            int per_sm = 0, nsm = 148;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fns[i], todo[i]->jit_threads,
+                                                          todo[i]->jit_smem);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            const uint64_t grid = (uint64_t)std::max(1, per_sm) * nsm;
+            todo[i]->jit_grid = (unsigned)std::min<uint64_t>(grid, todo[i]->ntiles);
+        }
     }
     return SV_OK;
 }
 
 cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream) {
     void* args[] = {&psi};
-    return cudaLaunchKernel(pp.jit_fn, dim3((unsigned)pp.ntiles), dim3((unsigned)pp.jit_threads), args,
-                            pp.jit_smem, stream);
+    const unsigned grid = pp.jit_persistent ? pp.jit_grid : (unsigned)pp.ntiles;
+    return cudaLaunchKernel(pp.jit_fn, dim3(grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem, stream);
 }
 
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {
