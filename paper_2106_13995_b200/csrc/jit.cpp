@@ -34,6 +34,8 @@ namespace {
 struct Em {
     std::ostringstream o;
     bool dbl = false;
+    std::map<std::string, std::string> rk;  // per-thread run-time constants already declared
+    int nvar = 0;
 
     std::string lit(double v) const {
         char b[64];
@@ -118,22 +120,65 @@ std::string scaled(const Em& e, const std::string& v, const cd& c) {
     return "mk(" + p.first + "," + p.second + ")";
 }
 
-// out_r = sum_c M[r][c] in_c for a d x d matrix over registers idx[0..d-1]
-void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M) {
+// ---- run-time signs (packed backend).  A -1 chosen by an index bit that is not a register
+// bit (CZ / Z on thread or tile-base qubits) is a per-thread value sg = (+-1, +-1).  It is
+// kept pending per register like the unit phases and folded into the next reader as the
+// multiplier of an FFMA2/FMUL2 (free when the reader is a butterfly); products with matrix
+// entries are per-thread constants declared once.
+std::string rt_const(Em& e, double k, const std::string& r) {
+    if (k == 1.0) return r;
+    if (k == -1.0) return "N(" + r + ")";
+    const std::string key = r + "|" + k2(k, k);
+    auto it = e.rk.find(key);
+    if (it != e.rk.end()) return it->second;
+    const std::string name = "rk" + std::to_string(e.nvar++);
+    e.o << "const C " << name << "=M(" << r << "," << k2(k, k) << ");";
+    e.rk.emplace(key, name);
+    return name;
+}
+
+// acc + c * r * v with a run-time sign r (empty r: f2_term)
+std::string f2_term_rt(Em& e, const std::string& acc, const std::string& v, const cd& c, const std::string& r) {
+    if (r.empty()) return f2_term(acc, v, c);
+    const double cr = c.real(), ci = c.imag();
+    auto fm = [&](const std::string& u, const std::string& k) {
+        return acc.empty() ? "M(" + u + "," + k + ")" : "F(" + u + "," + k + "," + acc + ")";
+    };
+    if (ci == 0.0 && std::abs(cr) == 1.0) return fm(cr > 0 ? v : "N(" + v + ")", r);
+    if (cr == 0.0 && std::abs(ci) == 1.0) return fm(ci > 0 ? "I(" + v + ")" : "NI(" + v + ")", r);
+    if (ci == 0.0) return fm(v, rt_const(e, cr, r));
+    if (cr == 0.0) return fm("I(" + v + ")", rt_const(e, ci, r));
+    const std::string kr = rt_const(e, cr, r), ki = rt_const(e, ci, r);
+    const std::string inner = acc.empty() ? "M(" + v + "," + kr + ")" : "F(" + v + "," + kr + "," + acc + ")";
+    return "F(I(" + v + ")," + ki + "," + inner + ")";
+}
+
+// out_r = sum_c M[r][c] in_c for a d x d matrix over registers idx[0..d-1]; rs: run-time
+// signs of the inputs (packed backend), cleared for the outputs
+void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M, std::vector<std::string>* rs = nullptr) {
     const size_t d = idx.size();
-    e.o << "{";
-    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
-    for (size_t r = 0; r < d; ++r) {
-        if (!e.dbl) {
+    if (!e.dbl) {
+        std::vector<std::string> ex(d);  // build first: run-time constants are declared outside the block
+        for (size_t r = 0; r < d; ++r) {
             std::string acc;
             for (size_t c = 0; c < d; ++c) {
                 const cd m = M[r * d + c];
                 if (is0(m)) continue;
-                acc = f2_term(acc, "i" + std::to_string(c), m);
+                acc = f2_term_rt(e, acc, "i" + std::to_string(c), m, rs ? (*rs)[idx[c]] : std::string());
             }
-            e.o << reg(idx[r]) << "=" << (acc.empty() ? std::string("0ull") : acc) << ";";
-            continue;
+            ex[r] = acc.empty() ? std::string("0ull") : acc;
         }
+        e.o << "{";
+        for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+        for (size_t r = 0; r < d; ++r) e.o << reg(idx[r]) << "=" << ex[r] << ";";
+        e.o << "}\n";
+        if (rs)
+            for (size_t c = 0; c < d; ++c) (*rs)[idx[c]].clear();
+        return;
+    }
+    e.o << "{";
+    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+    for (size_t r = 0; r < d; ++r) {
         std::string re, im;
         for (size_t c = 0; c < d; ++c) {
             const cd m = M[r * d + c];
@@ -194,21 +239,56 @@ using Pend = std::map<int, std::pair<cd, cd>>;
 //           own, it is folded into the next op that reads the register (a column of its
 //           matrix, or an operand modifier of the packed FP32 instruction), so those diagonal
 //           gates cost no instruction at all.
+//   rs   -- per-register pending run-time sign (name of a per-thread +-1 pair, packed backend)
 struct PassState {
     cd fac = 1;
     Pend pend;
     std::vector<cd> ph;
+    std::vector<std::string> rs;
+    std::map<std::string, std::string> sgprod;  // products of run-time signs already declared
 };
 
 bool is_unit(const cd& c) {
     return c == cd(1, 0) || c == cd(-1, 0) || c == cd(0, 1) || c == cd(0, -1);
 }
 
-// multiply register s by its pending unit phase now
-void flush_ph(Em& e, PassState& ps, int s) {
-    if (is1(ps.ph[s])) return;
-    e.o << reg(s) << "=" << scaled(e, reg(s), ps.ph[s]) << ";";
+// c * (pending phase) * (pending run-time sign) * v, clearing both
+std::string take(Em& e, PassState& ps, int s, const cd& c) {
+    const cd k = c * ps.ph[s];
+    const std::string r = ps.rs[s];
     ps.ph[s] = 1;
+    ps.rs[s].clear();
+    return e.dbl ? scaled(e, reg(s), k) : f2_term_rt(e, "", reg(s), k, r);
+}
+
+// multiply register s by its pending unit phase and run-time sign now
+void flush_ph(Em& e, PassState& ps, int s) {
+    if (is1(ps.ph[s]) && ps.rs[s].empty()) return;
+    const std::string ex = take(e, ps, s, 1);
+    e.o << reg(s) << "=" << ex << ";";
+}
+
+// a new per-thread sign (+-1 by a run-time condition)
+std::string make_sign(Em& e, const std::string& cond, double c_true, double c_false) {
+    const std::string name = "sg" + std::to_string(e.nvar++);
+    e.o << "const C " << name << "=(" << cond << ")?" << k2(c_true, c_true) << ":" << k2(c_false, c_false) << ";";
+    return name;
+}
+
+void add_sign(Em& e, PassState& ps, int s, const std::string& sg) {
+    std::string& r = ps.rs[s];
+    if (r.empty()) {
+        r = sg;
+        return;
+    }
+    const std::string key = r + "*" + sg;
+    auto it = ps.sgprod.find(key);
+    if (it == ps.sgprod.end()) {
+        const std::string name = "sg" + std::to_string(e.nvar++);
+        e.o << "const C " << name << "=M(" << r << "," << sg << ");";
+        it = ps.sgprod.emplace(key, name).first;
+    }
+    r = it->second;
 }
 
 // multiply the registers by a pending per-qubit factor now (controlled ops on the qubit need it)
@@ -221,10 +301,13 @@ void emit_flush(Em& e, const StageCtx& sc, PassState& ps, int q) {
     const int pq = sc.pos[q];
     if (pq >= 0) {
         for (int s = 0; s < R; ++s) {
-            const cd c = (((s >> pq) & 1) ? s1 : s0) * ps.ph[s];
-            ps.ph[s] = 1;
-            if (is1(c)) continue;
-            e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
+            const cd c = ((s >> pq) & 1) ? s1 : s0;
+            if (is1(c * ps.ph[s]) && ps.rs[s].empty()) {
+                ps.ph[s] = 1;
+                continue;
+            }
+            const std::string ex = take(e, ps, s, c);
+            e.o << reg(s) << "=" << ex << ";";
         }
         e.o << "\n";
     } else {
@@ -270,13 +353,12 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
         if (cm || pq < 0) {
             std::string cond = cm ? "((g&" + std::to_string(cm) + "ull)==" + std::to_string(cm) + "ull)" : "true";
             if (pq < 0) cond += "&&((g>>" + std::to_string(q) + ")&1ull)";
-            e.o << "{const C sg=(" << cond << ")?" << k2(-1, -1) << ":" << k2(1, 1) << ";";
+            const std::string sg = make_sign(e, cond, -1, 1);
             for (int s : touched) {
                 if (pq >= 0 && !((s >> pq) & 1)) continue;
-                e.o << reg(s) << "=M(" << scaled(e, reg(s), ps.ph[s]) << ",sg);";
-                ps.ph[s] = 1;
+                add_sign(e, ps, s, sg);  // pending: folded into the next reader
             }
-            e.o << "}\n";
+            e.o << "\n";
             return;
         }
     }
@@ -346,21 +428,27 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
                     e.o << "{";
                     for (int c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
                     std::vector<cd> nph(d);
+                    std::vector<std::string> nrs(d);
                     for (int r = 0; r < d; ++r)
                         for (int c = 0; c < d; ++c)
                             if (is1(M[r * d + c])) {
                                 e.o << reg(idx[r]) << "=i" << c << ";";
                                 nph[r] = ps.ph[idx[c]];
+                                nrs[r] = ps.rs[idx[c]];
                             }
-                    for (int r = 0; r < d; ++r) ps.ph[idx[r]] = nph[r];
+                    for (int r = 0; r < d; ++r) {
+                        ps.ph[idx[r]] = nph[r];
+                        ps.rs[idx[r]] = nrs[r];
+                    }
                     e.o << "}\n";
                 } else {
-                    // fold the inputs' pending phases into the matrix columns
+                    // fold the inputs' pending phases into the matrix columns (and their
+                    // run-time signs into the multipliers)
                     std::vector<cd> Mp = M;
                     for (int c = 0; c < d; ++c)
                         for (int r = 0; r < d; ++r) Mp[r * d + c] *= ps.ph[idx[c]];
                     for (int c = 0; c < d; ++c) ps.ph[idx[c]] = 1;
-                    emit_dense(e, idx, Mp);
+                    emit_dense(e, idx, Mp, &ps.rs);
                 }
             }
         } break;
@@ -387,15 +475,11 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
             const bool real_signs = c0.imag() == 0.0 && c1.imag() == 0.0 && std::abs(c0.real()) == 1.0 &&
                                     std::abs(c1.real()) == 1.0;
             if (q >= 0 && pq < 0 && !e.dbl && real_signs && !cm) {
-                // +-1 chosen by a non-register index bit: one branch-free FMUL2 per amplitude
-                // (the register's pending unit phase rides along as an operand modifier)
-                e.o << "{const C sg=((g>>" << q << ")&1ull)?" << k2(c1.real(), c1.real()) << ":"
-                    << k2(c0.real(), c0.real()) << ";";
-                for (int s : touched) {
-                    e.o << reg(s) << "=M(" << scaled(e, reg(s), ps.ph[s]) << ",sg);";
-                    ps.ph[s] = 1;
-                }
-                e.o << "}\n";
+                // +-1 chosen by a non-register index bit: a pending run-time sign
+                const std::string sg =
+                    make_sign(e, "((g>>" + std::to_string(q) + ")&1ull)", c1.real(), c0.real());
+                for (int s : touched) add_sign(e, ps, s, sg);
+                e.o << "\n";
             } else if (q >= 0 && pq < 0) {
                 // factor chosen by an index bit that is not a register bit
                 for (int s : touched) flush_ph(e, ps, s);
@@ -410,14 +494,18 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
                 e.o << "}\n";
             } else {
                 for (int s : touched) {
-                    const cd c = ((pq < 0) ? c0 : (((s >> pq) & 1) ? c1 : c0)) * ps.ph[s];
+                    const cd cb = (pq < 0) ? c0 : (((s >> pq) & 1) ? c1 : c0);
+                    const cd c = cb * ps.ph[s];
                     if (is_unit(c) && !cm) {
                         ps.ph[s] = c;  // +-1, +-i: defer, folded into the next reader
                         continue;
                     }
-                    ps.ph[s] = 1;
-                    if (is1(c)) continue;
-                    e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
+                    if (is1(c) && ps.rs[s].empty()) {
+                        ps.ph[s] = 1;
+                        continue;
+                    }
+                    const std::string ex = take(e, ps, s, cb);
+                    e.o << reg(s) << "=" << ex << ";";
                 }
                 e.o << "\n";
             }
@@ -598,6 +686,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     const std::string SM = pf ? "bc" : "sm";
     PassState ps;
     ps.ph.assign(R, cd(1, 0));
+    ps.rs.assign(R, std::string());
     for (size_t si = first; si < sym.stages.size(); ++si) {
         const StageSym& st = sym.stages[si];
         StageCtx sc;
@@ -647,10 +736,11 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             for (int q : rt) emit_flush(e, sc, ps, q);
             o << "// deferred factors of the pass (scalar, per register qubit, per register)\n";
             for (int s = 0; s < R; ++s) {
-                cd c = ps.fac * ps.ph[s];
+                cd c = ps.fac;
                 for (auto& kv : ps.pend) c *= ((s >> sc.pos[kv.first]) & 1) ? kv.second.second : kv.second.first;
-                if (is1(c)) continue;
-                o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
+                if (is1(c * ps.ph[s]) && ps.rs[s].empty()) continue;
+                const std::string ex = take(e, ps, s, c);
+                o << reg(s) << "=" << ex << ";";
             }
             o << "\n";
             if (!sym.out_perm.empty()) {
