@@ -127,14 +127,32 @@ std::string scaled(const Em& e, const std::string& v, const cd& c) {
 // entries are per-thread constants declared once.
 std::string rt_const(Em& e, double k, const std::string& r) {
     if (k == 1.0) return r;
-    if (k == -1.0) return "N(" + r + ")";
-    const std::string key = r + "|" + k2(k, k);
+    if (k == -1.0) return e.dbl ? "(-" + r + ")" : "N(" + r + ")";
+    const std::string key = r + "|" + (e.dbl ? e.lit(k) : k2(k, k));
     auto it = e.rk.find(key);
     if (it != e.rk.end()) return it->second;
     const std::string name = "rk" + std::to_string(e.nvar++);
-    e.o << "const C " << name << "=M(" << r << "," << k2(k, k) << ");";
+    if (e.dbl) e.o << "const R " << name << "=" << r << "*" << e.lit(k) << ";";
+    else e.o << "const C " << name << "=M(" << r << "," << k2(k, k) << ");";
     e.rk.emplace(key, name);
     return name;
+}
+
+// scalar backend: (re, im) of c * r * v with a run-time sign r (a double +-1)
+std::pair<std::string, std::string> mul_rt(Em& e, const std::string& v, const cd& c, const std::string& r) {
+    if (r.empty()) return mul(e, v, c);
+    const double cr = c.real(), ci = c.imag();
+    const std::string x = v + ".x", y = v + ".y";
+    if (ci == 0.0) {
+        const std::string k = rt_const(e, cr, r);
+        return {x + "*" + k, y + "*" + k};
+    }
+    if (cr == 0.0) {
+        const std::string k = rt_const(e, ci, r);
+        return {"(-" + y + ")*" + k, x + "*" + k};
+    }
+    const std::string kr = rt_const(e, cr, r), ki = rt_const(e, ci, r);
+    return {x + "*" + kr + "-" + y + "*" + ki, x + "*" + ki + "+" + y + "*" + kr};
 }
 
 // acc + c * r * v with a run-time sign r (empty r: f2_term)
@@ -176,21 +194,25 @@ void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M, st
             for (size_t c = 0; c < d; ++c) (*rs)[idx[c]].clear();
         return;
     }
-    e.o << "{";
-    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+    std::vector<std::string> ex(d);  // built first: run-time constants are declared outside the block
     for (size_t r = 0; r < d; ++r) {
         std::string re, im;
         for (size_t c = 0; c < d; ++c) {
             const cd m = M[r * d + c];
             if (is0(m)) continue;
-            auto p = mul(e, "i" + std::to_string(c), m);
+            auto p = mul_rt(e, "i" + std::to_string(c), m, rs ? (*rs)[idx[c]] : std::string());
             re += (re.empty() ? "" : "+") + p.first;
             im += (im.empty() ? "" : "+") + p.second;
         }
         if (re.empty()) { re = e.lit(0.0); im = e.lit(0.0); }
-        e.o << reg(idx[r]) << "=mk(" << re << "," << im << ");";
+        ex[r] = "mk(" + re + "," + im + ")";
     }
+    e.o << "{";
+    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+    for (size_t r = 0; r < d; ++r) e.o << reg(idx[r]) << "=" << ex[r] << ";";
     e.o << "}\n";
+    if (rs)
+        for (size_t c = 0; c < d; ++c) (*rs)[idx[c]].clear();
 }
 
 // unscaled form M' and deferred factor f with U = f M' (no controls only)
@@ -258,7 +280,11 @@ std::string take(Em& e, PassState& ps, int s, const cd& c) {
     const std::string r = ps.rs[s];
     ps.ph[s] = 1;
     ps.rs[s].clear();
-    return e.dbl ? scaled(e, reg(s), k) : f2_term_rt(e, "", reg(s), k, r);
+    if (e.dbl) {
+        auto p = mul_rt(e, reg(s), k, r);
+        return "mk(" + p.first + "," + p.second + ")";
+    }
+    return f2_term_rt(e, "", reg(s), k, r);
 }
 
 // multiply register s by its pending unit phase and run-time sign now
@@ -271,7 +297,8 @@ void flush_ph(Em& e, PassState& ps, int s) {
 // a new per-thread sign (+-1 by a run-time condition)
 std::string make_sign(Em& e, const std::string& cond, double c_true, double c_false) {
     const std::string name = "sg" + std::to_string(e.nvar++);
-    e.o << "const C " << name << "=(" << cond << ")?" << k2(c_true, c_true) << ":" << k2(c_false, c_false) << ";";
+    if (e.dbl) e.o << "const R " << name << "=(" << cond << ")?" << e.lit(c_true) << ":" << e.lit(c_false) << ";";
+    else e.o << "const C " << name << "=(" << cond << ")?" << k2(c_true, c_true) << ":" << k2(c_false, c_false) << ";";
     return name;
 }
 
@@ -285,7 +312,8 @@ void add_sign(Em& e, PassState& ps, int s, const std::string& sg) {
     auto it = ps.sgprod.find(key);
     if (it == ps.sgprod.end()) {
         const std::string name = "sg" + std::to_string(e.nvar++);
-        e.o << "const C " << name << "=M(" << r << "," << sg << ");";
+        if (e.dbl) e.o << "const R " << name << "=" << r << "*" << sg << ";";
+        else e.o << "const C " << name << "=M(" << r << "," << sg << ");";
         it = ps.sgprod.emplace(key, name).first;
     }
     r = it->second;
@@ -347,7 +375,7 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
         if (sel(s)) touched.push_back(s);
     // Branch-free sign flips: a diagonal op with factor -1 (Z, CZ, CCZ, ...) whose condition
     // involves non-register bits becomes one FMUL2 by a per-thread sign per affected register.
-    if (!e.dbl && k == 0 && (op.kind == OP_Z || (op.kind == OP_PHASE && op.coef[0] == cd(-1, 0))) &&
+    if (k == 0 && (op.kind == OP_Z || (op.kind == OP_PHASE && op.coef[0] == cd(-1, 0))) &&
         op.dq.size() == 1) {
         const int q = op.dq[0], pq = sc.pos[q];
         if (cm || pq < 0) {
@@ -474,7 +502,7 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
             }
             const bool real_signs = c0.imag() == 0.0 && c1.imag() == 0.0 && std::abs(c0.real()) == 1.0 &&
                                     std::abs(c1.real()) == 1.0;
-            if (q >= 0 && pq < 0 && !e.dbl && real_signs && !cm) {
+            if (q >= 0 && pq < 0 && real_signs && !cm) {
                 // +-1 chosen by a non-register index bit: a pending run-time sign
                 const std::string sg =
                     make_sign(e, "((g>>" + std::to_string(q) + ")&1ull)", c1.real(), c0.real());

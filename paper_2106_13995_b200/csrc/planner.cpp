@@ -53,7 +53,14 @@ uint64_t qmask(const std::vector<int>& qs) {
 
 }  // namespace
 
-int default_rb(bool dbl, int nl) { return std::max(1, std::min(dbl ? 4 : 5, nl)); }
+int default_rb(bool dbl, int nl) {
+    static const int env = [] {
+        const char* e = getenv("SV_RB");
+        return e ? atoi(e) : 0;
+    }();
+    const int rb = (env >= 1 && env <= 5) ? env : (dbl ? 4 : 5);
+    return std::max(1, std::min(rb, nl));
+}
 
 namespace {
 template <typename real>
