@@ -51,6 +51,32 @@ def test_24q_supremacy_d20_full_state_vs_oracle(P):
         assert_close(got, ref, dtype, W.gate_count(c))
 
 
+@pytest.mark.parametrize("n", [33, 34])
+def test_beyond_2_32_amplitudes(P, n):
+    """R22: 64-bit offsets past 2^32 amplitudes on one GPU (33q c64 = 64 GiB, 34q = 128 GiB):
+    a GHZ-like state across the top qubits, closed form; then a mirror circuit returns |0>."""
+    top, mid = n - 1, n - 2
+    text = (f"qubits: {n}\nX {top}\nH {mid}\nCNOT {mid},0\nCNOT {mid},{n - 3}\nT {mid}\nH {top}\n")
+    h = 2 ** -0.5
+    with P.StateVector(n, "c64") as sv:
+        sv.apply_circuit(text)
+        # X(top) H(mid) CNOT CNOT T(mid) H(top): amplitudes on |top in {0,1}> x {|0>, |mid,n-3,0>}
+        base1 = (1 << mid) | (1 << (n - 3)) | 1
+        t = np.exp(1j * np.pi / 4)
+        expect = {0: h * h, 1 << top: -h * h, base1: h * h * t, base1 | (1 << top): -h * h * t}
+        for idx, val in expect.items():
+            got = complex(sv.amplitudes(idx, 1)[0])
+            assert abs(got - val) <= 1e-6, (idx, got, val)
+        assert abs(sv.norm() - 1) <= 1e-6
+        p = sv.probabilities([top, mid])
+        assert np.max(np.abs(p - 0.25)) <= 1e-6
+    c = W.supremacy(7, 5, 4, seed=2, n=n)
+    with P.StateVector(n, "c64") as sv:
+        sv.apply_circuit(W.to_text(W.concat(c, W.inverse(c))))
+        assert abs(complex(sv.amplitudes(0, 1)[0]) - 1) <= 1e-4
+        assert abs(sv.norm() - 1) <= 1e-4
+
+
 def test_31q_multiplier_basis_exact(P):
     """Config 4 at full width (8x7 multiplier, c64): basis inputs map exactly to the oracle's
     classical image (bit-level evaluator), amplitude exactly 1, norm exactly 1 (R10)."""
