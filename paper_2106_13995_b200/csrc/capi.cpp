@@ -201,7 +201,7 @@ sv_status plan_schedule(sv_plan_s* p) {
         const sv_status st = lower_gate(p->circ.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
         if (st != SV_OK) return fail(st, err);
     }
-    const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err);
+    const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err, &p->circ);
     if (st != SV_OK) return fail(st, err);
     // a reversible circuit: one gather pass, unless its scattered reads cost more than the
     // fused tile passes (both estimated in HBM passes)
@@ -478,7 +478,8 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     int threads;
     size_t smem;
     bool pers;
-    if (pp.kind == PassPlan::TILE && pp.sym) src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers);
+    int tpc;
+    if (pp.kind == PassPlan::TILE && pp.sym) src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers, tpc);
     else if (pp.kind == PassPlan::PERM) src = gen_perm_source(pp, pp.perm_dbl, threads);
     if (len) *len = src.size();
     if (buf && cap) {
@@ -689,20 +690,33 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
     for (int j = 0; j < nql; ++j) P.sorted[j] = so[j];
     P.smask = 0;
     for (int j = 0; j < nql; ++j) P.smask |= 1ull << so[j];
+    P.nl = s->nl;
     const uint64_t rest = 1ull << (s->nl - nql);
     P.per_chunk = std::min<uint64_t>(rest, 1ull << 13);
     P.chunks = rest / P.per_chunk;
     const uint64_t nk = 1ull << nql;
     const int shards = shard_count(s);
     // partials: per-chunk trees (nk x chunks) or per-bin chunks of >= 64 rest indices
-    const uint64_t nparts = nk * std::max<uint64_t>(P.chunks, std::max<uint64_t>(1, rest / 64));
+    const uint64_t nparts = marginal_partials(P);
     sv_status st = ensure_scratch(s, nparts + nk * shards);
     if (st != SV_OK) return st;
     double* partial = s->d_scratch;
     double* outs = s->d_scratch + nparts;
+    // one shard, no subset qubit among the rank bits: the final kernel stores the bins in the
+    // caller's order and they go straight to host_out
+    const bool direct = shards == 1 && (s->virt || s->world == 1) && gq.empty();
+    if (direct) {
+        P.remap = 1;
+        for (int j = 0; j < nql; ++j) P.outpos[j] = lj[j];
+    }
     for (int i = 0; i < shards; ++i) {
         cudaError_t e = launch_marginal(s->dbl, s->shard_ptr(i), P, partial, outs + nk * i, s->stream);
         if (e != cudaSuccess) return cuda_fail(e, "marginal");
+    }
+    if (direct) {
+        CK(cudaMemcpyAsync(host_out, outs, nk * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        return SV_OK;
     }
     std::vector<double> loc(nk * shards);
     CK(cudaMemcpyAsync(loc.data(), outs, nk * shards * sizeof(double), cudaMemcpyDeviceToHost, s->stream));

@@ -76,6 +76,7 @@ sv_status lower_gate(const Gate& g, int gi, const Context& ctx, const RunOpts& o
 struct StageSym {
     std::vector<int> rq;         // physical qubit of register bit j (size rb)
     std::vector<LOp> ops;        // in application order
+    std::vector<int> lane_first; // optional: tile qubits taking the lowest thread bits, in order
 };
 
 struct TileSym {                 // symbolic tile pass: what both backends execute
@@ -119,8 +120,10 @@ struct Schedule {
     std::vector<int> end_phys;   // qubit map after the schedule if it changes the layout (else empty)
 };
 
+// `circ` (optional) enables layout relabelling: the remaining gates are re-lowered under the
+// map each pass leaves behind (single GPU, generated kernels).
 sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,
-                         std::string& err);
+                         std::string& err, const Circuit* circ = nullptr);
 
 // if every gate is a classical reversible gate (X / SWAP with any controls)
 // and the state is 10..32 qubits on one GPU, the whole circuit becomes one PERM pass.

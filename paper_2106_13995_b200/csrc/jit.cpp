@@ -21,6 +21,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <algorithm>
 #include <sstream>
 #include <thread>
 #include <unordered_map>
@@ -171,83 +172,6 @@ std::string f2_term_rt(Em& e, const std::string& acc, const std::string& v, cons
     return "F(I(" + v + ")," + ki + "," + inner + ")";
 }
 
-// out_r = sum_c M[r][c] in_c for a d x d matrix over registers idx[0..d-1]; rs: run-time
-// signs of the inputs (packed backend), cleared for the outputs
-void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M, std::vector<std::string>* rs = nullptr) {
-    const size_t d = idx.size();
-    if (!e.dbl) {
-        std::vector<std::string> ex(d);  // build first: run-time constants are declared outside the block
-        for (size_t r = 0; r < d; ++r) {
-            std::string acc;
-            for (size_t c = 0; c < d; ++c) {
-                const cd m = M[r * d + c];
-                if (is0(m)) continue;
-                acc = f2_term_rt(e, acc, "i" + std::to_string(c), m, rs ? (*rs)[idx[c]] : std::string());
-            }
-            ex[r] = acc.empty() ? std::string("0ull") : acc;
-        }
-        e.o << "{";
-        for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
-        for (size_t r = 0; r < d; ++r) e.o << reg(idx[r]) << "=" << ex[r] << ";";
-        e.o << "}\n";
-        if (rs)
-            for (size_t c = 0; c < d; ++c) (*rs)[idx[c]].clear();
-        return;
-    }
-    std::vector<std::string> ex(d);  // built first: run-time constants are declared outside the block
-    for (size_t r = 0; r < d; ++r) {
-        std::string re, im;
-        for (size_t c = 0; c < d; ++c) {
-            const cd m = M[r * d + c];
-            if (is0(m)) continue;
-            auto p = mul_rt(e, "i" + std::to_string(c), m, rs ? (*rs)[idx[c]] : std::string());
-            re += (re.empty() ? "" : "+") + p.first;
-            im += (im.empty() ? "" : "+") + p.second;
-        }
-        if (re.empty()) { re = e.lit(0.0); im = e.lit(0.0); }
-        ex[r] = "mk(" + re + "," + im + ")";
-    }
-    e.o << "{";
-    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
-    for (size_t r = 0; r < d; ++r) e.o << reg(idx[r]) << "=" << ex[r] << ";";
-    e.o << "}\n";
-    if (rs)
-        for (size_t c = 0; c < d; ++c) (*rs)[idx[c]].clear();
-}
-
-// unscaled form M' and deferred factor f with U = f M' (no controls only)
-bool unscaled(int kind, std::vector<cd>& M, cd& f) {
-    const cd I(0, 1);
-    const double r = 0.70710678118654752440;
-    switch (kind) {
-        case OP_H: M = {1, 1, 1, -1}; f = r; return true;
-        case OP_SX: M = {1, -I, -I, 1}; f = cd(.5, .5); return true;
-        case OP_SXDG: M = {1, I, I, 1}; f = cd(.5, -.5); return true;
-        case OP_SY: M = {1, -1, 1, 1}; f = cd(.5, .5); return true;
-        case OP_SYDG: M = {1, 1, -1, 1}; f = cd(.5, -.5); return true;
-        case OP_X: M = {0, 1, 1, 0}; f = 1; return true;
-        case OP_Y: M = {0, -I, I, 0}; f = 1; return true;
-        default: return false;
-    }
-}
-
-cd diag_const(int kind) {
-    const double r = 0.70710678118654752440;
-    switch (kind) {
-        case OP_Z: return -1;
-        case OP_S: return cd(0, 1);
-        case OP_SDG: return cd(0, -1);
-        case OP_T: return cd(r, r);
-        case OP_TDG: return cd(r, -r);
-        default: return 1;
-    }
-}
-
-struct StageCtx {
-    int rb;
-    int pos[64];  // physical qubit -> register position, -1 if not a register bit
-};
-
 // Pending per-qubit diagonal factors diag(s0, s1) not yet multiplied into the registers
 // (the 1/sqrt2 of T and Tdg).  They commute with every op except a non-diagonal op that
 // targets the qubit, which absorbs them into its matrix columns (its butterfly adds become
@@ -302,22 +226,111 @@ std::string make_sign(Em& e, const std::string& cond, double c_true, double c_fa
     return name;
 }
 
-void add_sign(Em& e, PassState& ps, int s, const std::string& sg) {
-    std::string& r = ps.rs[s];
-    if (r.empty()) {
-        r = sg;
-        return;
-    }
-    const std::string key = r + "*" + sg;
+// product of two run-time signs (empty = +1), declared once per pass
+std::string sign_mul(Em& e, PassState& ps, const std::string& a, const std::string& b) {
+    if (a.empty()) return b;
+    if (b.empty()) return a;
+    if (a == b) return std::string();
+    const std::string key = a < b ? a + "*" + b : b + "*" + a;
     auto it = ps.sgprod.find(key);
     if (it == ps.sgprod.end()) {
         const std::string name = "sg" + std::to_string(e.nvar++);
-        if (e.dbl) e.o << "const R " << name << "=" << r << "*" << sg << ";";
-        else e.o << "const C " << name << "=M(" << r << "," << sg << ");";
+        if (e.dbl) e.o << "const R " << name << "=" << a << "*" << b << ";";
+        else e.o << "const C " << name << "=M(" << a << "," << b << ");";
         it = ps.sgprod.emplace(key, name).first;
     }
-    r = it->second;
+    return it->second;
 }
+
+void add_sign(Em& e, PassState& ps, int s, const std::string& sg) { ps.rs[s] = sign_mul(e, ps, ps.rs[s], sg); }
+
+// out_r = sum_c M[r][c] in_c for a d x d matrix over registers idx[0..d-1].  Run-time signs
+// of the inputs (ps non-null): the most common one stays pending on every output, the others
+// enter the multipliers relative to it (free when all inputs carry the same sign).
+void emit_dense(Em& e, const std::vector<int>& idx, const std::vector<cd>& M, PassState* ps = nullptr) {
+    const size_t d = idx.size();
+    std::vector<std::string> rel(d);
+    std::string common;
+    if (ps) {
+        std::map<std::string, int> cnt;
+        for (size_t c = 0; c < d; ++c) cnt[ps->rs[idx[c]]]++;
+        int best = -1;
+        for (auto& kv : cnt)
+            if (kv.second > best) { best = kv.second; common = kv.first; }
+        for (size_t c = 0; c < d; ++c) rel[c] = sign_mul(e, *ps, common, ps->rs[idx[c]]);
+    }
+    if (!e.dbl) {
+        std::vector<std::string> ex(d);  // build first: run-time constants are declared outside the block
+        for (size_t r = 0; r < d; ++r) {
+            std::string acc;
+            for (size_t c = 0; c < d; ++c) {
+                const cd m = M[r * d + c];
+                if (is0(m)) continue;
+                acc = f2_term_rt(e, acc, "i" + std::to_string(c), m, rel[c]);
+            }
+            ex[r] = acc.empty() ? std::string("0ull") : acc;
+        }
+        e.o << "{";
+        for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+        for (size_t r = 0; r < d; ++r) e.o << reg(idx[r]) << "=" << ex[r] << ";";
+        e.o << "}\n";
+        if (ps)
+            for (size_t c = 0; c < d; ++c) ps->rs[idx[c]] = common;
+        return;
+    }
+    std::vector<std::string> ex(d);  // built first: run-time constants are declared outside the block
+    for (size_t r = 0; r < d; ++r) {
+        std::string re, im;
+        for (size_t c = 0; c < d; ++c) {
+            const cd m = M[r * d + c];
+            if (is0(m)) continue;
+            auto p = mul_rt(e, "i" + std::to_string(c), m, rel[c]);
+            re += (re.empty() ? "" : "+") + p.first;
+            im += (im.empty() ? "" : "+") + p.second;
+        }
+        if (re.empty()) { re = e.lit(0.0); im = e.lit(0.0); }
+        ex[r] = "mk(" + re + "," + im + ")";
+    }
+    e.o << "{";
+    for (size_t c = 0; c < d; ++c) e.o << "const C i" << c << "=" << reg(idx[c]) << ";";
+    for (size_t r = 0; r < d; ++r) e.o << reg(idx[r]) << "=" << ex[r] << ";";
+    e.o << "}\n";
+    if (ps)
+        for (size_t c = 0; c < d; ++c) ps->rs[idx[c]] = common;
+}
+
+// unscaled form M' and deferred factor f with U = f M' (no controls only)
+bool unscaled(int kind, std::vector<cd>& M, cd& f) {
+    const cd I(0, 1);
+    const double r = 0.70710678118654752440;
+    switch (kind) {
+        case OP_H: M = {1, 1, 1, -1}; f = r; return true;
+        case OP_SX: M = {1, -I, -I, 1}; f = cd(.5, .5); return true;
+        case OP_SXDG: M = {1, I, I, 1}; f = cd(.5, -.5); return true;
+        case OP_SY: M = {1, -1, 1, 1}; f = cd(.5, .5); return true;
+        case OP_SYDG: M = {1, 1, -1, 1}; f = cd(.5, -.5); return true;
+        case OP_X: M = {0, 1, 1, 0}; f = 1; return true;
+        case OP_Y: M = {0, -I, I, 0}; f = 1; return true;
+        default: return false;
+    }
+}
+
+cd diag_const(int kind) {
+    const double r = 0.70710678118654752440;
+    switch (kind) {
+        case OP_Z: return -1;
+        case OP_S: return cd(0, 1);
+        case OP_SDG: return cd(0, -1);
+        case OP_T: return cd(r, r);
+        case OP_TDG: return cd(r, -r);
+        default: return 1;
+    }
+}
+
+struct StageCtx {
+    int rb;
+    int pos[64];  // physical qubit -> register position, -1 if not a register bit
+};
 
 // multiply the registers by a pending per-qubit factor now (controlled ops on the qubit need it)
 void emit_flush(Em& e, const StageCtx& sc, PassState& ps, int q) {
@@ -330,12 +343,10 @@ void emit_flush(Em& e, const StageCtx& sc, PassState& ps, int q) {
     if (pq >= 0) {
         for (int s = 0; s < R; ++s) {
             const cd c = ((s >> pq) & 1) ? s1 : s0;
-            if (is1(c * ps.ph[s]) && ps.rs[s].empty()) {
-                ps.ph[s] = 1;
-                continue;
-            }
-            const std::string ex = take(e, ps, s, c);
-            e.o << reg(s) << "=" << ex << ";";
+            const cd k = c * ps.ph[s];
+            ps.ph[s] = 1;
+            if (is1(k)) continue;
+            e.o << reg(s) << "=" << scaled(e, reg(s), k) << ";";  // run-time sign stays pending
         }
         e.o << "\n";
     } else {
@@ -476,7 +487,7 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
                     for (int c = 0; c < d; ++c)
                         for (int r = 0; r < d; ++r) Mp[r * d + c] *= ps.ph[idx[c]];
                     for (int c = 0; c < d; ++c) ps.ph[idx[c]] = 1;
-                    emit_dense(e, idx, Mp, &ps.rs);
+                    emit_dense(e, idx, Mp, &ps);
                 }
             }
         } break;
@@ -528,12 +539,10 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
                         ps.ph[s] = c;  // +-1, +-i: defer, folded into the next reader
                         continue;
                     }
-                    if (is1(c) && ps.rs[s].empty()) {
-                        ps.ph[s] = 1;
-                        continue;
-                    }
-                    const std::string ex = take(e, ps, s, cb);
-                    e.o << reg(s) << "=" << ex << ";";
+                    ps.ph[s] = 1;
+                    if (is1(c)) continue;
+                    // a pending run-time sign commutes with the factor: it stays pending
+                    e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
                 }
                 e.o << "\n";
             }
@@ -595,6 +604,33 @@ bool prefetch_enabled() {
     return b;
 }
 
+bool scalar_fma() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SCALAR_FMA");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
+// tiles per CTA: the CTA's warps run the same stage code in step (one instruction-cache
+// footprint per SM instead of one per resident CTA)
+int tiles_per_cta() {
+    static const int v = [] {
+        const char* e = getenv("SV_TPC");
+        return e ? std::max(1, atoi(e)) : 1;
+    }();
+    return v;
+}
+
+// CTAs per SM the register allocation must allow (SV_MIN_WARPS: resident warps per SM)
+int min_blocks(int threads) {
+    static const int w = [] {
+        const char* e = getenv("SV_MIN_WARPS");
+        return e ? atoi(e) : 16;
+    }();
+    return std::max(1, std::min(32, w * 32 / threads));
+}
+
 // run-length emission of  sum_i ((t >> i) & 1) << dst[i]
 std::string deposit_expr(const std::vector<int>& dst, bool wide) {
     std::string ex;
@@ -618,18 +654,26 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 
 }  // namespace
 
-std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent) {
+std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
+                            int& tpc) {
     Em e;
     e.dbl = sym.dbl;
     const int rb = sym.rb, R = 1 << rb;
     const int m = (int)sym.tq.size();
     const int tb = m - rb;
-    threads = 1 << tb;
+    const int tthreads = 1 << tb;  // threads per tile
     const bool multi = sym.stages.size() > 1;
-    const bool pf = prefetch_enabled() && sym.out_perm.empty() && m >= (sym.dbl ? 4 : 5) + 1 &&
-                    ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)threads == 0;
+    const bool pf = prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
+                    ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)tthreads == 0;
     persistent = pf;
-    smem = pf ? 2 * ((size_t)1 << m) * (sym.dbl ? 16 : 8) : multi ? ((size_t)1 << m) * (sym.dbl ? 16 : 8) : 0;
+    const size_t tile_bytes = ((size_t)1 << m) * (sym.dbl ? 16 : 8);
+    tpc = 1;
+    if (!pf)
+        while (tpc * 2 <= tiles_per_cta() && ntiles % (uint64_t)(tpc * 2) == 0 && tthreads * tpc * 2 <= 1024 &&
+               (!multi || tile_bytes * tpc * 2 <= (size_t)200 * 1024))
+            tpc *= 2;
+    threads = tthreads * tpc;
+    smem = pf ? 2 * tile_bytes : multi ? tile_bytes * tpc : 0;
     int local_of[64];
     for (int i = 0; i < 64; ++i) local_of[i] = -1;
     for (int b = 0; b < m; ++b) local_of[sym.tq[b]] = b;
@@ -649,10 +693,14 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
              "DI float hi(C a){float x,y;asm(\"mov.b64 {%0,%1},%2;\":\"=f\"(x),\"=f\"(y):\"l\"(a));return y;}\n"
              "DI C A(C a,C b){C d;asm(\"add.rn.f32x2 %0,%1,%2;\":\"=l\"(d):\"l\"(a),\"l\"(b));return d;}\n"
              "DI C M(C a,C b){C d;asm(\"mul.rn.f32x2 %0,%1,%2;\":\"=l\"(d):\"l\"(a),\"l\"(b));return d;}\n"
-             "DI C F(C a,C b,C c){C d;asm(\"fma.rn.f32x2 %0,%1,%2,%3;\":\"=l\"(d):\"l\"(a),\"l\"(b),\"l\"(c));return d;}\n"
+             "DI C F2(C a,C b,C c){C d;asm(\"fma.rn.f32x2 %0,%1,%2,%3;\":\"=l\"(d):\"l\"(a),\"l\"(b),\"l\"(c));return d;}\n"
+             "DI C F1(C a,C b,C c){return pk(fmaf(lo(a),lo(b),lo(c)),fmaf(hi(a),hi(b),hi(c)));}\n"
              "DI C N(C a){return pk(-lo(a),-hi(a));}\n"
              "DI C I(C a){return pk(-hi(a),lo(a));}\n"
              "DI C NI(C a){return pk(hi(a),-lo(a));}\n";
+        // FFMA2 issues at 1/3 per cycle on B200, two scalar FFMAs at 1 each
+        // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes
+        o << (scalar_fma() ? "#define F F1\n" : "#define F F2\n");
     }
     // pf: persistent CTAs; the next tile is prefetched into the second shared-memory buffer
     // with cp.async while this one is computed (HBM reads overlap the arithmetic)
@@ -661,16 +709,19 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (pf)
         while (first + 1 < sym.stages.size() && sym.stages[first].ops.empty()) ++first;  // I/O-only stage
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
-      << (pf ? 1 : threads >= 512 ? 1 : threads >= 256 ? 2 : 4) << ") svpass(C* __restrict__ psi){\n";
-    if (multi || pf) o << "extern __shared__ C sm[];\n";
-    o << "const unsigned t=threadIdx.x;\n";
+      << (pf ? 1 : min_blocks(threads)) << ") svpass(C* __restrict__ psi){\n";
+    if (pf) o << "extern __shared__ C sm[];\n";
+    else if (multi && tpc > 1) o << "extern __shared__ C sm_[];\nC* sm=sm_+((threadIdx.x>>" << tb << ")<<" << m << ");\n";
+    else if (multi) o << "extern __shared__ C sm[];\n";
+    if (tpc > 1) o << "const unsigned t=threadIdx.x&" << (tthreads - 1) << "u;\n";
+    else o << "const unsigned t=threadIdx.x;\n";
     o << "C v[" << R << "];\nunsigned long long g,base;\n";
     if (multi || pf) o << "unsigned tl;\n";
     const int L = sym.dbl ? 4 : 5;  // the tile's low qubits 0..L-1 are contiguous in memory
     if (pf) {
         const int E = sym.dbl ? 1 : 2;  // elements per 16-byte chunk
         const uint64_t chunks = ((uint64_t)1 << m) / E;
-        const int cpt = (int)(chunks / threads);
+        const int cpt = (int)(chunks / tthreads);
         auto dep = [&](uint64_t x) {  // tile-local element index -> global offset
             uint64_t r = x & ((1ull << L) - 1);
             for (int b = L; b < m; ++b)
@@ -705,7 +756,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         o << "asm volatile(\"cp.async.wait_group 1;\"); __syncthreads();\n";
         o << "base=tile;\n";
     } else {
-        o << "base=blockIdx.x;\n";
+        if (tpc > 1) o << "base=(unsigned long long)blockIdx.x*" << tpc << "u+(threadIdx.x>>" << tb << ");\n";
+        else o << "base=blockIdx.x;\n";
     }
     for (int b = 0; b < m; ++b) {
         const int q = sym.tq[b];
@@ -724,6 +776,18 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         std::vector<int> tq_phys, tq_local;
         for (int b = 0; b < m; ++b)
             if (sc.pos[sym.tq[b]] < 0) { tq_phys.push_back(sym.tq[b]); tq_local.push_back(b); }
+        if (!st.lane_first.empty()) {
+            // the stage's lowest thread bits take these qubits (the store's coalesced lanes)
+            std::vector<int> p2, l2;
+            for (int q : st.lane_first) { p2.push_back(q); l2.push_back(local_of[q]); }
+            for (size_t i = 0; i < tq_phys.size(); ++i)
+                if (std::find(st.lane_first.begin(), st.lane_first.end(), tq_phys[i]) == st.lane_first.end()) {
+                    p2.push_back(tq_phys[i]);
+                    l2.push_back(tq_local[i]);
+                }
+            tq_phys = p2;
+            tq_local = l2;
+        }
         o << "// stage " << si << ": registers";
         for (int q : st.rq) o << " " << q;
         o << "\n";
@@ -758,10 +822,28 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         for (const LOp& op : st.ops) emit_op(e, op, sc, ps);
         if (si + 1 == sym.stages.size()) {
             // pending factors of non-register qubits need the index bit: apply them first
+            // (real ones join one per-thread scale, multiplied in with the deferred factor)
             std::vector<int> rt;
-            for (auto& kv : ps.pend)
-                if (sc.pos[kv.first] < 0) rt.push_back(kv.first);
+            std::string rscale;
+            for (auto& kv : ps.pend) {
+                if (sc.pos[kv.first] >= 0) continue;
+                const cd s0 = kv.second.first, s1 = kv.second.second;
+                if (s0.imag() == 0.0 && s1.imag() == 0.0) {
+                    const std::string k = "ks" + std::to_string(e.nvar++);
+                    const std::string cond = "((g>>" + std::to_string(kv.first) + ")&1ull)";
+                    if (e.dbl) o << "const R " << k << "=" << cond << "?" << e.lit(s1.real()) << ":" << e.lit(s0.real()) << ";";
+                    else o << "const C " << k << "=" << cond << "?" << k2(s1.real(), s1.real()) << ":" << k2(s0.real(), s0.real()) << ";";
+                    rscale = sign_mul(e, ps, rscale, k);
+                } else {
+                    rt.push_back(kv.first);
+                }
+            }
+            for (auto it = ps.pend.begin(); it != ps.pend.end();)
+                if (sc.pos[it->first] < 0 && std::find(rt.begin(), rt.end(), it->first) == rt.end()) it = ps.pend.erase(it);
+                else ++it;
             for (int q : rt) emit_flush(e, sc, ps, q);
+            if (!rscale.empty())
+                for (int s = 0; s < R; ++s) ps.rs[s] = sign_mul(e, ps, ps.rs[s], rscale);
             o << "// deferred factors of the pass (scalar, per register qubit, per register)\n";
             for (int s = 0; s < R; ++s) {
                 cd c = ps.fac;
@@ -944,8 +1026,10 @@ sv_status jit_prepare(Schedule& sc, std::string& err) {
             todo[i]->jit_smem = 0;
             todo[i]->ntiles = ((1ull << todo[i]->m) >> 5) / (uint64_t)todo[i]->jit_threads;
         } else {
+            int tpc = 1;
             srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->ntiles, todo[i]->jit_threads, todo[i]->jit_smem,
-                                      todo[i]->jit_persistent);
+                                      todo[i]->jit_persistent, tpc);
+            todo[i]->jit_grid = (unsigned)(todo[i]->ntiles / (uint64_t)tpc);
         }
     }
     std::vector<sv_status> st(todo.size(), SV_OK);
@@ -982,7 +1066,7 @@ sv_status jit_prepare(Schedule& sc, std::string& err) {
 
 cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream) {
     void* args[] = {&psi};
-    const unsigned grid = pp.jit_persistent ? pp.jit_grid : (unsigned)pp.ntiles;
+    const unsigned grid = pp.jit_grid;
     return cudaLaunchKernel(pp.jit_fn, dim3(grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem, stream);
 }
 

@@ -7,7 +7,8 @@
 namespace svb {
 
 // CUDA source of one fused tile pass; returns the launch shape.
-std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent);
+std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
+                            int& tpc);
 // Compile (or fetch from the in-process cache) and return a CUfunction.
 sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::string& err);
 // Compile every TILE pass of a schedule that has no kernel yet (parallel over passes).

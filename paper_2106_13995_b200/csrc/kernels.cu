@@ -15,6 +15,7 @@
 // sum-over-ops flops; it is HBM-bound while its per-amplitude op cost stays below the
 // FP32 (FP64) ridge.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 #include <utility>
@@ -470,17 +471,73 @@ __global__ void __launch_bounds__(256) marginal_bin_kernel(const typename V2<rea
     partial[chunk * nk + k] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
+// Wide subsets in any qubit layout: one warp per value of the subset bits above the lane
+// bits, its 32 lanes on index bits 0..4 (256 contiguous bytes per load), each lane summing
+// its rest indices of one chunk in a fixed order; lanes that differ only in rest bits are then
+// combined by xor-shuffles (a + b == b + a: the same value on every lane, deterministic).
+// partial[chunk][k], k = subset bits in ascending position order.
+template <typename real>
+__global__ void __launch_bounds__(256) marginal_lane_kernel(const typename V2<real>::t* __restrict__ psi,
+                                                            MarginalParams P, uint64_t per, double* __restrict__ partial) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nk = 1ull << P.nq;
+    const uint64_t hmask = P.smask & ~31ull;              // subset bits held by the warp index
+    const uint64_t rmask = ((1ull << P.nl) - 1) & ~P.smask & ~31ull;  // rest bits walked by the loop
+    if (w >> __popcll(hmask)) return;
+    uint64_t hb = 0, x = w;
+    for (int b = 5; b < P.nl; ++b)
+        if ((hmask >> b) & 1) { hb |= (x & 1ull) << b; x >>= 1; }
+    uint64_t cur = 0, r0 = blockIdx.y * per;
+    for (int b = 5; b < P.nl && r0; ++b)
+        if ((rmask >> b) & 1) { cur |= (r0 & 1ull) << b; r0 >>= 1; }
+    const uint64_t fixed = hb | lane;
+    const uint64_t skip = ~rmask;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (per >= 8) {
+        for (uint64_t r = 0; r < per; r += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const auto a = psi[cur | fixed];
+                acc[u] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+                cur = ((cur | skip) + 1) & rmask;
+            }
+        }
+    } else {
+        for (uint64_t r = 0; r < per; ++r) {
+            const auto a = psi[cur | fixed];
+            acc[r] += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+            cur = ((cur | skip) + 1) & rmask;
+        }
+    }
+    double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    for (int b = 0; b < 5; ++b)
+        if (!((P.smask >> b) & 1)) v += __shfl_xor_sync(0xffffffffu, v, 1 << b);
+    if (lane & ~(unsigned)P.smask & 31u) return;
+    uint64_t k = 0;
+    for (int j = 0; j < P.nq; ++j) k |= ((fixed >> P.sorted[j]) & 1ull) << j;
+    partial[blockIdx.y * nk + k] = v;
+}
+
+__device__ __forceinline__ uint64_t out_index(const MarginalParams& P, uint64_t k) {
+    if (!P.remap) return k;
+    uint64_t o = 0;
+    for (int j = 0; j < P.nq; ++j) o |= ((k >> j) & 1ull) << P.outpos[j];
+    return o;
+}
+
 __global__ void __launch_bounds__(256) marginal_bin_final_kernel(const double* __restrict__ partial, uint64_t nk,
-                                                                 uint64_t chunks, double* __restrict__ out) {
+                                                                 uint64_t chunks, double* __restrict__ out,
+                                                                 MarginalParams P) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= nk) return;
     double acc = 0.0;
     for (uint64_t c = 0; c < chunks; ++c) acc += partial[c * nk + k];
-    out[k] = acc;
+    out[out_index(P, k)] = acc;
 }
 
 __global__ void __launch_bounds__(256) marginal_final_kernel(const double* __restrict__ partial, uint64_t chunks,
-                                                             double* __restrict__ out) {
+                                                             double* __restrict__ out, MarginalParams P) {
     __shared__ double red[256];
     const uint64_t k = blockIdx.x;
     double acc = 0.0;
@@ -491,7 +548,7 @@ __global__ void __launch_bounds__(256) marginal_final_kernel(const double* __res
         if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[k] = red[0];
+    if (threadIdx.x == 0) out[out_index(P, k)] = red[0];
 }
 
 // ------------------------------------------------------------------ host launchers
@@ -562,9 +619,47 @@ cudaError_t launch_fill(bool dbl, void* psi, uint64_t N, double re, double im, c
     return cudaGetLastError();
 }
 
+// marginal_lane_kernel geometry: warps (subset values above the lane bits), rest indices per
+// chunk, chunks; the rest walk is chunked so that >= ~64K warps run (grid.y stays in range)
+static void lane_split(const MarginalParams& P, uint64_t& warps, uint64_t& per, uint64_t& chunks2) {
+    warps = 1ull << (P.nq - __builtin_popcountll(P.smask & 31ull));
+    const uint64_t rest = 1ull << (P.nl - 5 - __builtin_popcountll(P.smask & ~31ull));
+    per = rest;
+    while (per > 8 && warps * (rest / per) < 65536) per /= 2;
+    while (rest / per > 32768) per *= 2;
+    chunks2 = rest / per;
+}
+
+uint64_t marginal_partials(const MarginalParams& P) {
+    const uint64_t nk = 1ull << P.nq;
+    if (P.nq >= 12 && P.nl >= 5) {
+        uint64_t warps, per, chunks2;
+        lane_split(P, warps, per, chunks2);
+        const uint64_t rest = P.chunks * P.per_chunk;
+        return nk * std::max<uint64_t>({chunks2, P.chunks, std::max<uint64_t>(1, rest / 64)});
+    }
+    return nk * std::max<uint64_t>(P.chunks, 1);
+}
+
 cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, double* partial, double* out,
                             cudaStream_t st) {
     const uint64_t nk = 1ull << P.nq;
+    bool sorted_q = true;
+    for (int j = 0; j < P.nq; ++j) sorted_q &= P.q[j] == P.sorted[j];
+    if (P.nq >= 12 && P.nl >= 5 && sorted_q) {
+        uint64_t warps, per, chunks2;
+        lane_split(P, warps, per, chunks2);
+        const unsigned threads = (unsigned)std::min<uint64_t>(256, warps * 32);
+        const dim3 grid((unsigned)((warps * 32 + threads - 1) / threads), (unsigned)chunks2);
+        if (dbl)
+            marginal_lane_kernel<double><<<grid, threads, 0, st>>>(reinterpret_cast<const double2*>(psi), P, per, partial);
+        else
+            marginal_lane_kernel<float><<<grid, threads, 0, st>>>(reinterpret_cast<const float2*>(psi), P, per, partial);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        marginal_bin_final_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(partial, nk, chunks2, out, P);
+        return cudaGetLastError();
+    }
     if (P.nq >= 12 && P.chunks * P.per_chunk >= 8) {
         // partial needs chunks2 * nk doubles: the caller sizes it as nk * P.chunks (>= this)
         const uint64_t rest = P.chunks * P.per_chunk;
@@ -578,7 +673,7 @@ cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, 
             marginal_bin_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(psi), P, per, partial);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        marginal_bin_final_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(partial, nk, chunks2, out);
+        marginal_bin_final_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(partial, nk, chunks2, out, P);
         return cudaGetLastError();
     }
     const uint64_t blocks = nk * P.chunks;
@@ -593,7 +688,7 @@ cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, 
     (void)threads;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    marginal_final_kernel<<<(unsigned)nk, 256, 0, st>>>(partial, P.chunks, out);
+    marginal_final_kernel<<<(unsigned)nk, 256, 0, st>>>(partial, P.chunks, out, P);
     return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@
 // commutes gates on disjoint qubits (reading R21).  Inside a pass, gates are cut into
 // register stages of RB qubits the same way.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -401,7 +402,7 @@ std::vector<cd> swap_bits_u2(const std::vector<cd>& M) {
 // the other needed qubits, then padding with the highest free tile qubits so the low qubits
 // stay lane bits for coalescing).
 bool make_sym(const std::vector<const LOp*>& ops, const std::vector<StagePlan>& stages, uint64_t S, int rb,
-              bool dbl, TileSym& sym, std::string& err) {
+              bool dbl, TileSym& sym, std::string& err, bool check_last = true) {
     sym.tq.clear();
     for (int q = 0; q < 64; ++q)
         if ((S >> q) & 1) sym.tq.push_back(q);
@@ -438,7 +439,7 @@ bool make_sym(const std::vector<const LOp*>& ops, const std::vector<StagePlan>& 
     };
     if (m >= rb + cl) {
         if (bad(sym.stages.front())) sym.stages.insert(sym.stages.begin(), io_stage());
-        if (bad(sym.stages.back())) sym.stages.push_back(io_stage());
+        if (check_last && bad(sym.stages.back())) sym.stages.push_back(io_stage());
     }
     return true;
 }
@@ -597,8 +598,9 @@ double pass_budget() {
 
 }  // namespace
 
-sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpts& o, Schedule& out,
-                         std::string& err) {
+sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const RunOpts& o, Schedule& out,
+                         std::string& err, const Circuit* circ) {
+    Context ctx = ctx_in;
     const bool dbl = ctx.dbl;
     const int nl = ctx.nl;
     const int rb = default_rb(dbl, nl);
@@ -606,18 +608,53 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
         const char* e = getenv("SV_TILE_QUBITS");
         return e ? atoi(e) : 0;
     }();
-    int m_max = o.tile_qubits > 0 ? o.tile_qubits : env_tile > 0 ? env_tile : default_tile_qubits(dbl, nl, rb);
-    // generated kernels take up to 512 threads per tile, the interpreter 256
-    m_max = std::max(rb, std::min({m_max, rb + (o.use_jit() ? 9 : 8), nl, kMaxTileQubits}));
     const int m_pad = std::min(rb + 8, nl);       // single-stage passes: 256 threads
     const int L = std::min(dbl ? 4 : 5, nl);      // low qubits: contiguous 256-byte runs
     const uint64_t lowmask = (L >= 64) ? ~0ull : ((1ull << L) - 1);
     const bool per_gate = !o.fuse || o.force_kernel == SV_KERNEL_PER_GATE || o.force_kernel == SV_KERNEL_DENSE;
+    // Relabelling (single GPU, generated kernels): the pass stores its tile with a permutation
+    // that brings the qubits the next pass wants into the low physical positions, so a tile
+    // is no longer forced to spend L of its m qubits on whatever sits at the bottom.
+    static const bool relabel_env = [] {
+        const char* e = getenv("SV_RELABEL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    const bool relabel = circ && relabel_env && o.use_jit() && !per_gate && ctx.world == 1 && nl >= m_pad &&
+                         nl >= L + 5;
+    // With relabelling a smaller tile wins (tools/sweep_relabel.sh, profiles/r01_relabel_sweep.txt):
+    // passes are FP-pipe bound and 4 CTAs per SM overlap their HBM phases better than 2.
+    int m_def = default_tile_qubits(dbl, nl, rb);
+    if (relabel) m_def = std::min(m_def, dbl ? 11 : 12);
+    int m_max = o.tile_qubits > 0 ? o.tile_qubits : env_tile > 0 ? env_tile : m_def;
+    // generated kernels take up to 512 threads per tile, the interpreter 256
+    m_max = std::max(rb, std::min({m_max, rb + (o.use_jit() ? 9 : 8), nl, kMaxTileQubits}));
+    std::vector<int> rem_gates;
+    if (circ)
+        for (size_t i = 0; i < circ->gates.size(); ++i) rem_gates.push_back((int)i);
 
-    std::vector<int> remaining(ops.size());
-    for (size_t i = 0; i < ops.size(); ++i) {
-        remaining[i] = (int)i;
-        if ((int)ops[i].tq.size() > rb) ops[i].densek = true;  // cannot live in registers
+    std::vector<int> remaining;
+    auto set_remaining_all = [&]() {
+        remaining.resize(ops.size());
+        for (size_t i = 0; i < ops.size(); ++i) {
+            remaining[i] = (int)i;
+            if ((int)ops[i].tq.size() > rb) ops[i].densek = true;  // cannot live in registers
+        }
+    };
+    auto relower = [&]() -> sv_status {  // ops of the remaining gates under the current map
+        ops.clear();
+        for (int gi : rem_gates) {
+            bool needs = false;
+            const sv_status r = lower_gate(circ->gates[gi], gi, ctx, o, ops, needs, err);
+            if (r != SV_OK) return r;
+        }
+        set_remaining_all();
+        return SV_OK;
+    };
+    if (circ) {
+        const sv_status r = relower();
+        if (r != SV_OK) return r;
+    } else {
+        set_remaining_all();
     }
 
     auto emit_dense = [&](const LOp& op) {
@@ -626,22 +663,16 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
         else write_dense_params<float>(op, ctx, pp);
         out.passes.push_back(std::move(pp));
     };
-
-    while (!remaining.empty()) {
-        // ---- choose the pass's gates and tile qubits
-        std::vector<int> pass_ops, deferred;
-        uint64_t S = lowmask;
+    // choose the pass's gates and tile qubits, starting from tile qubits S0; `order` records
+    // the order in which qubits joined the tile
+    auto select = [&](const std::vector<int>& rem, uint64_t S0, std::vector<int>& pass_ops, std::vector<int>& deferred,
+                      std::vector<int>* order) -> uint64_t {
+        uint64_t S = S0;
         Blocker blocked;
         size_t ncoef = 0;
         double cost = 0;
         const double budget = o.use_jit() ? pass_budget() : 1e30;
-        const LOp& first = ops[remaining[0]];
-        if (first.densek) {
-            emit_dense(first);
-            remaining.erase(remaining.begin());
-            continue;
-        }
-        for (int idx : remaining) {
+        for (int idx : rem) {
             const LOp& op = ops[idx];
             const bool full = per_gate ? !pass_ops.empty()
                                        : (pass_ops.size() >= (size_t)kMaxOps ||
@@ -654,6 +685,9 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
             }
             const uint64_t need = S | qmask(op.tq);
             if (popc(need) <= m_max && (int)op.tq.size() <= rb) {
+                if (order)
+                    for (int q : op.tq)
+                        if (!((S >> q) & 1)) order->push_back(q);
                 S = need;
                 pass_ops.push_back(idx);
                 ncoef += coef_size(op);
@@ -663,6 +697,24 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                 blocked.add(op);
             }
         }
+        return S;
+    };
+
+    while (!remaining.empty()) {
+        std::vector<int> pass_ops, deferred;
+        const LOp& first = ops[remaining[0]];
+        if (first.densek) {
+            emit_dense(first);
+            if (circ) {
+                rem_gates.erase(std::find(rem_gates.begin(), rem_gates.end(), first.gate));
+                const sv_status r = relower();
+                if (r != SV_OK) return r;
+            } else {
+                remaining.erase(remaining.begin());
+            }
+            continue;
+        }
+        uint64_t S = select(remaining, lowmask, pass_ops, deferred, nullptr);
         // ---- cut the pass into register stages
         std::vector<StagePlan> stages;
         std::vector<int> todo(pass_ops.size());
@@ -777,21 +829,115 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx, const RunOpt
                 if (!used && !((lowmask >> q) & 1)) S &= ~(1ull << q);
             }
         }
+        std::vector<int> next = deferred;
+        next.insert(next.end(), leftover.begin(), leftover.end());
+        std::sort(next.begin(), next.end());
+        // ---- relabel: which tile qubits should sit at the bottom for the next pass
+        std::vector<int> perm;  // physical position -> position after this pass (tile-internal)
+        std::vector<int> lowset;
+        if (relabel && !next.empty()) {
+            // the L tile qubits that, sitting at the bottom, let the next pass take the most
+            // work (every L-subset of the tile when affordable; ties keep qubits in place)
+            std::vector<int> tqs;
+            for (int q = 0; q < 64; ++q)
+                if ((S >> q) & 1) tqs.push_back(q);
+            const int nt = (int)tqs.size();
+            double best = -1;
+            uint64_t bestmask = lowmask;
+            auto score_of = [&](uint64_t low) {
+                std::vector<int> pn, dn;
+                select(next, low, pn, dn, nullptr);
+                double sc = 0;
+                for (int i : pn) sc += op_cost(ops[i]);
+                return sc + 1e-6 * popc(low & lowmask);
+            };
+            if (nt <= 20) {
+                uint32_t c = (1u << L) - 1;
+                while (c < (1u << nt)) {
+                    uint64_t low = 0;
+                    for (int j = 0; j < nt; ++j)
+                        if ((c >> j) & 1) low |= 1ull << tqs[j];
+                    const double sc = score_of(low);
+                    if (sc > best) { best = sc; bestmask = low; }
+                    const uint32_t u = c & (0u - c), w = c + u;
+                    c = w | (((w ^ c) >> 2) / u);
+                }
+            }
+            for (int q = 0; q < 64; ++q)
+                if ((bestmask >> q) & 1) lowset.push_back(q);
+            perm.resize(64);
+            for (int q = 0; q < 64; ++q) perm[q] = q;
+            std::vector<int> free_slots;
+            for (int slot = 0; slot < L; ++slot)
+                if (std::find(lowset.begin(), lowset.end(), slot) == lowset.end()) free_slots.push_back(slot);
+            size_t fi = 0;
+            bool moved = false;
+            for (int q : lowset) {
+                if (q < L) continue;
+                const int slot = free_slots[fi++];
+                perm[q] = slot;
+                perm[slot] = q;
+                moved = true;
+            }
+            if (!moved) perm.clear();
+        }
+        if (getenv("SV_PLAN_DEBUG")) {
+            fprintf(stderr, "pass %zu: ops %zu deferred %zu S=", out.passes.size(), pass_ops.size(), next.size());
+            for (int q = 0; q < 64; ++q) if ((S >> q) & 1) fprintf(stderr, "%d ", q);
+            fprintf(stderr, "| low ->");
+            for (int q : lowset) fprintf(stderr, " %d", q);
+            fprintf(stderr, " stages %zu\n", stages.size());
+        }
         std::vector<const LOp*> pops;  // stage op indices refer to this list
         for (int idx : pass_ops) pops.push_back(&ops[idx]);
         PassPlan pp;
         pp.sym = std::make_shared<TileSym>();
-        if (!make_sym(pops, stages, S, rb, dbl, *pp.sym, err)) return SV_ERR_STATE;
+        if (!make_sym(pops, stages, S, rb, dbl, *pp.sym, err, perm.empty())) return SV_ERR_STATE;
+        if (!perm.empty()) {
+            TileSym& sym = *pp.sym;
+            // the qubits landing at the bottom must be the store's lanes, in output order
+            std::vector<int> lanes(L);
+            for (int q = 0; q < 64; ++q)
+                if (((S >> q) & 1) && perm[q] < L) lanes[perm[q]] = q;
+            auto conflicts = [&](const StageSym& st) {
+                for (int q : st.rq)
+                    if (std::find(lanes.begin(), lanes.end(), q) != lanes.end()) return true;
+                return false;
+            };
+            // a single stage would load and store through the same lanes: split it
+            if (sym.stages.size() == 1 || conflicts(sym.stages.back())) {
+                StageSym io;
+                for (int b = (int)sym.tq.size() - 1; b >= 0 && (int)io.rq.size() < rb; --b)
+                    if (std::find(lanes.begin(), lanes.end(), sym.tq[b]) == lanes.end()) io.rq.push_back(sym.tq[b]);
+                sym.stages.push_back(io);
+            }
+            sym.stages.back().lane_first = lanes;
+            sym.out_perm = perm;
+        }
         const bool ok = dbl ? write_tile_params<double>(*pp.sym, ctx, pp, err)
                             : write_tile_params<float>(*pp.sym, ctx, pp, err);
         if (!ok) return SV_ERR_STATE;
         out.stages += pp.sym->stages.size();
         out.passes.push_back(std::move(pp));
         // ---- next round: leftovers and deferred gates in original order
-        std::vector<int> next = deferred;
-        next.insert(next.end(), leftover.begin(), leftover.end());
-        std::sort(next.begin(), next.end());
-        remaining = std::move(next);
+        if (circ) {
+            std::vector<int> g2;
+            for (int idx : next) g2.push_back(ops[idx].gate);
+            std::sort(g2.begin(), g2.end());
+            g2.erase(std::unique(g2.begin(), g2.end()), g2.end());
+            rem_gates = g2;
+            if (!perm.empty())
+                for (int& p : ctx.phys) p = perm[p];
+            const sv_status r = relower();
+            if (r != SV_OK) return r;
+        } else {
+            remaining = std::move(next);
+        }
+    }
+    if (circ) {
+        bool ident = true;
+        for (int q = 0; q < (int)ctx.phys.size(); ++q) ident &= ctx.phys[q] == ctx_in.phys[q];
+        if (!ident) out.end_phys = ctx.phys;
     }
     return SV_OK;
 }

@@ -31,8 +31,12 @@ struct MarginalParams {
     uint64_t smask;        // bit mask of the subset qubits
     uint64_t chunks;       // chunks of the rest space per k
     uint64_t per_chunk;    // rest indices per chunk
+    int nl;                // local qubits (index bits of the state buffer)
+    int remap;             // nonzero: the final kernels store bin k at sum_j bit_j(k) << outpos[j]
+    int outpos[28];
 };
 
+uint64_t marginal_partials(const MarginalParams& P);  // partial-sum doubles launch_marginal needs
 cudaError_t launch_tile_pass(bool dbl, int rb, void* psi, const void* params, int m, int nstages, uint64_t ntiles,
                              cudaStream_t st);
 cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t groups, cudaStream_t st);

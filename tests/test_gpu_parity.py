@@ -226,6 +226,27 @@ def test_readout_probabilities_norm(P, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_wide_marginals_relabelled_layout(P, dtype):
+    """Wide subsets (>= 12 qubits: the lane kernel) on a state left in a relabelled physical
+    layout by the plan: orders, subsets without the low qubits, all qubits."""
+    n = 20
+    c = W.supremacy(5, 4, 12, seed=3)
+    text = W.to_text(c)
+    ref = oracle.simulate(text)
+    rng = np.random.default_rng(5)
+    subsets = [list(range(n)), list(range(4, 20)), list(range(19, 5, -1)),
+               [int(x) for x in rng.permutation(n)[:14]], [0, 2, 4, 6, 8, 10, 12, 14, 16, 18, 1, 3]]
+    tol = 1e-12 if dtype == "c128" else 1e-6
+    with P.StateVector(n, dtype) as sv:
+        sv.apply_circuit(text)
+        assert sv.qubit_map() != list(range(n))  # the plan left a relabelled layout
+        for qs in subsets:
+            got = sv.probabilities(qs)
+            assert np.max(np.abs(got - oracle.probabilities(ref, qs))) <= tol, qs
+            assert np.array_equal(got, sv.probabilities(qs))  # deterministic
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_init_states(P, dtype):
     for n in (1, 7, 20):
         with P.StateVector(n, dtype) as sv:

@@ -1,0 +1,75 @@
+// Throughput of the FP32 forms the generated passes use (B200): warp instructions per cycle
+// per SM for FADD/FFMA (register and immediate forms) and the paired FADD2/FFMA2/FMUL2.
+#include <cstdio>
+#include <cuda_runtime.h>
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 A(u64 a, u64 b) { u64 d; asm volatile("add.rn.f32x2 %0,%1,%2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ u64 F(u64 a, u64 b, u64 c) { u64 d; asm volatile("fma.rn.f32x2 %0,%1,%2,%3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+__device__ __forceinline__ u64 M(u64 a, u64 b) { u64 d; asm volatile("mul.rn.f32x2 %0,%1,%2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+#define NCH 8
+#define ITER 4096
+template <int MODE>
+__global__ void k(u64* out, u64 seed, float fs) {
+    u64 v[NCH];
+    float f[NCH];
+    double dd[NCH];
+    for (int i = 0; i < NCH; ++i) { v[i] = seed + i + threadIdx.x; f[i] = fs + i + threadIdx.x; dd[i] = f[i]; }
+    const double ds = fs * 0.5;
+    const u64 kk = seed * 3;
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+            if (MODE == 0) v[i] = A(v[i], kk);
+            if (MODE == 1) v[i] = F(v[i], kk, v[(i + 1) % NCH]);
+            if (MODE == 2) v[i] = M(v[i], kk);
+            if (MODE == 3) f[i] = f[i] * fs + f[(i + 1) % NCH];
+            if (MODE == 4) f[i] = f[i] * 1.0001f + 0.5f;
+            if (MODE == 5) f[i] = f[i] + fs;
+            if (MODE == 8) v[i] = F(v[i], 0x3f3504f33f3504f3ull, v[(i + 1) % NCH]);
+            if (MODE == 9) v[i] = F(v[i], 0x3f3504f33f3504f3ull, v[i]);
+            if (MODE == 6) dd[i] = dd[i] + dd[(i + 1) % NCH];
+            if (MODE == 7) dd[i] = dd[i] * ds + dd[(i + 1) % NCH];
+        }
+    }
+    u64 s = 0;
+    float t = 0;
+    for (int i = 0; i < NCH; ++i) { s ^= v[i]; t += f[i] + (float)dd[i]; }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s ^ (u64)__float_as_uint(t);
+}
+template <int MODE>
+void run(const char* name, u64* d) {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int clk;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    const int threads = 512, blocks = sms * 4;
+    k<MODE><<<blocks, threads>>>(d, 1, 1.f);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    k<MODE><<<blocks, threads>>>(d, 1, 1.f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double winstr = (double)blocks * threads / 32 * ITER * NCH;
+    const double cycles = ms * 1e-3 * clk * 1e3;
+    printf("%-22s %.3f ms  warp-instr/cycle/SM %.3f (per SMSP %.3f)\n", name, ms, winstr / cycles / sms,
+           winstr / cycles / sms / 4);
+}
+int main() {
+    u64* d;
+    cudaMalloc(&d, 148 * 4 * 512 * 8 * 2);
+    run<0>("FADD2 (reg)", d);
+    run<1>("FFMA2 (reg)", d);
+    run<2>("FMUL2 (reg)", d);
+    run<3>("FFMA (reg)", d);
+    run<4>("FFMA (imm)", d);
+    run<5>("FADD (reg)", d);
+    run<8>("FFMA2 (imm, 2 regs)", d);
+    run<9>("FFMA2 (imm, same reg)", d);
+    run<6>("DADD (reg)", d);
+    run<7>("DFMA (reg)", d);
+    return 0;
+}

@@ -20,6 +20,8 @@ ap.add_argument("--fuse", type=int, default=1)
 a = ap.parse_args()
 if a.workload == "supremacy":
     c = W.supremacy(6, 5, 20, 0) if a.qubits == 30 else W.supremacy((a.qubits + 4) // 5, 5, 20, 0, n=a.qubits)
+elif a.workload == "qft":
+    c = W.qft(a.qubits)
 else:
     c = W.multiplier(8, 7)
 plan = P.Plan(W.to_text(c), a.dtype, fuse=bool(a.fuse))

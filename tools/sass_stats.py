@@ -49,7 +49,11 @@ with tempfile.TemporaryDirectory() as d:
         n = len(ops)
         fp = sum(cnt[k] for k in ("FADD", "FFMA", "FMUL", "DADD", "DFMA", "DMUL", "FADD2", "FFMA2", "FMUL2"))
         R = 1 << rb
+        # FP pipe cycles per warp on one SMSP (B200, tools/micro/fp_rate.cu): FADD2/FMUL2 2,
+        # FFMA2 3, scalar FP32 1, DADD/DMUL 2, DFMA 2.2
+        pipe = (2 * (cnt["FADD2"] + cnt["FMUL2"]) + 3 * cnt["FFMA2"] + cnt["FADD"] + cnt["FFMA"] + cnt["FMUL"]
+                + 2 * (cnt["DADD"] + cnt["DMUL"]) + 2.2 * cnt["DFMA"])
         tot.update(cnt)
         print(f"pass {i}: {hdr[24:]}, regs {regs.group(1) if regs else '?'}, instr/thread {n}, "
-              f"instr/amp {n / R:.1f}, fp/amp {fp / R:.1f}, lds+sts {cnt['LDS'] + cnt['STS']}, "
-              f"bra {cnt['BRA']}")
+              f"instr/amp {n / R:.1f}, fp/amp {fp / R:.1f}, fp-pipe cyc/amp {pipe / R:.1f}, lds+sts {cnt['LDS'] + cnt['STS']}, "
+              f"bra {cnt['BRA']}, local {cnt['LDL'] + cnt['STL']}")
