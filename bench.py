@@ -433,7 +433,7 @@ def run_ours(args):
                 "stages_per_step": info.get("stages"),
                 "swaps_per_step": st.get("swaps", 0),
                 "state_bytes_per_gpu": local_amps * amp,
-                "timed": "init |0...0> + all tile passes (plan compiled once, outside the timed region)",
+                "timed": "init |0...0> (deferred, synthesised by the first pass) + all tile passes (plan compiled once, outside the timed region)",
                 "l2": "state (>= 8 GiB per GPU) is larger than L2 (126 MB): no flush needed",
                 "parallelism": f"sharded by top {world.bit_length() - 1} qubits" if world > 1 else "single GPU",
             },

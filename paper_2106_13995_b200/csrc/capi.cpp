@@ -131,7 +131,7 @@ int shard_count(const sv_state_s* s) { return s->virt ? s->world : 1; }
 int shard_rank(const sv_state_s* s, int i) { return s->virt ? i : s->rank; }
 
 sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stats* st,
-                       std::vector<cudaEvent_t>* ev = nullptr) {
+                       std::vector<cudaEvent_t>* ev = nullptr, int64_t basis = -1) {
     if (ev) {
         while (ev->size() < sc.passes.size() + 1) {
             cudaEvent_t x;
@@ -166,7 +166,9 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
                     e = cudaMemcpyAsync(psi, s->d2, bytes, cudaMemcpyDeviceToDevice, s->stream);
                 }
             }
-        } else if (pp.kind == PassPlan::TILE && pp.jit_fn)
+        } else if (pp.kind == PassPlan::TILE && pi == 1 && basis >= 0)
+            e = jit_launch_basis(pp, psi, (uint64_t)basis, s->stream);
+        else if (pp.kind == PassPlan::TILE && pp.jit_fn)
             e = jit_launch(pp, psi, s->stream);
         else if (pp.kind == PassPlan::TILE)
             e = launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles, s->stream);
@@ -178,7 +180,7 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
             st->passes += 1;
             st->launches += 1;
             st->stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
-            st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+            st->hbm_bytes += (pi == 1 && basis >= 0 ? 1ull : 2ull) * pp.touched_amps * s->amp_bytes();
         }
     }
     return SV_OK;
@@ -215,8 +217,39 @@ sv_status plan_schedule(sv_plan_s* p) {
     return SV_OK;
 }
 
+// Write the basis state |k> (all shards of this process).
+sv_status write_basis(sv_state_s* s, uint64_t k) {
+    s->lazy_basis = -1;
+    const size_t shard_bytes = (size_t)s->local_amps() * s->amp_bytes();
+    const int owner = (int)(k >> s->nl);
+    const uint64_t local = k & (s->local_amps() - 1);
+    for (int i = 0; i < shard_count(s); ++i) {
+        void* p = s->shard_ptr(i);
+        CK(cudaMemsetAsync(p, 0, shard_bytes, s->stream));
+        if (shard_rank(s, i) == owner) {
+            if (s->dbl) {
+                static const double one[2] = {1.0, 0.0};
+                CK(cudaMemcpyAsync((char*)p + local * 16, one, 16, cudaMemcpyHostToDevice, s->stream));
+            } else {
+                static const float one[2] = {1.0f, 0.0f};
+                CK(cudaMemcpyAsync((char*)p + local * 8, one, 8, cudaMemcpyHostToDevice, s->stream));
+            }
+        }
+    }
+    return SV_OK;
+}
+
+// Write a deferred basis-state initialisation now (before anything reads the buffer).
+sv_status materialize(sv_state_s* s) {
+    if (s->lazy_basis < 0) return SV_OK;
+    return write_basis(s, (uint64_t)s->lazy_basis);
+}
+
 // Make the qubit map the identity (sharded states after swaps); see sharded.cpp.
-sv_status canonicalize(sv_state_s* s) { return sharded_canonicalize(s); }
+sv_status canonicalize(sv_state_s* s) {
+    const sv_status st = materialize(s);
+    return st != SV_OK ? st : sharded_canonicalize(s);
+}
 
 }  // namespace
 
@@ -363,27 +396,16 @@ sv_status sv_init_basis(sv_state s, uint64_t k) {
     if (!s) return fail(SV_ERR_ARG, "NULL state");
     if (s->n < 64 && k >= (1ull << s->n)) return fail(SV_ERR_RANGE, "basis index out of range");
     for (int q = 0; q < s->n; ++q) s->phys[q] = q;
-    const size_t shard_bytes = (size_t)s->local_amps() * s->amp_bytes();
-    const int owner = (int)(k >> s->nl);
-    const uint64_t local = k & (s->local_amps() - 1);
-    for (int i = 0; i < shard_count(s); ++i) {
-        void* p = s->shard_ptr(i);
-        CK(cudaMemsetAsync(p, 0, shard_bytes, s->stream));
-        if (shard_rank(s, i) == owner) {
-            if (s->dbl) {
-                static const double one[2] = {1.0, 0.0};
-                CK(cudaMemcpyAsync((char*)p + local * 16, one, 16, cudaMemcpyHostToDevice, s->stream));
-            } else {
-                static const float one[2] = {1.0f, 0.0f};
-                CK(cudaMemcpyAsync((char*)p + local * 8, one, 8, cudaMemcpyHostToDevice, s->stream));
-            }
-        }
+    if (s->owned && s->world == 1 && !s->virt) {
+        s->lazy_basis = (int64_t)k;  // written by the next plan's first pass, or by materialize()
+        return SV_OK;
     }
-    return SV_OK;
+    return write_basis(s, k);
 }
 
 sv_status sv_init_uniform(sv_state s) {
     if (!s) return fail(SV_ERR_ARG, "NULL state");
+    s->lazy_basis = -1;
     for (int q = 0; q < s->n; ++q) s->phys[q] = q;
     const double a = uniform_amp(s->n);
     for (int i = 0; i < shard_count(s); ++i) {
@@ -417,6 +439,10 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
     if (!s || !mat || !targets || (ncontrols > 0 && !controls) || ncontrols < 0)
         return fail(SV_ERR_ARG, "sv_apply_gate: NULL argument");
     if (k < 1 || k > 5) return fail(SV_ERR_ARG, "sv_apply_gate: k must be in [1, 5]");
+    {
+        const sv_status st = materialize(s);
+        if (st != SV_OK) return st;
+    }
     Gate g;
     for (int j = 0; j < k; ++j) g.targets.push_back(targets[j]);
     for (int j = 0; j < ncontrols; ++j) g.controls.push_back(controls[j]);
@@ -548,9 +574,15 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
         if (st != SV_OK) return st;
     }
     if (!p->jitted && p->opts.use_jit()) {
-        const sv_status st = jit_prepare(p->sched, err);
+        const sv_status st = jit_prepare(p->sched, err, true);
         if (st != SV_OK) return fail(st, err);
         p->jitted = true;
+    }
+    // fused init: a deferred basis state is synthesised by the first pass instead of written
+    int64_t kb = -1;
+    if (s->lazy_basis >= 0 && !p->opts.use_graph && !p->sched.passes.empty() && p->sched.passes[0].jit_fn_basis) {
+        kb = s->lazy_basis;
+        s->lazy_basis = -1;  // the map is the identity after an init
     }
     sv_status st = canonicalize(s);  // the plan assumes the identity layout
     if (st != SV_OK) return st;
@@ -589,7 +621,7 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
             stats->hbm_bytes = 2ull * s->local_amps() * s->amp_bytes() * tmp.passes;
         }
     } else {
-        st = run_schedule(s, s->d, p->sched, stats, p->opts.profile ? &p->prof_ev : nullptr);
+        st = run_schedule(s, s->d, p->sched, stats, p->opts.profile ? &p->prof_ev : nullptr, kb);
         p->prof_n = p->opts.profile ? (int)p->sched.passes.size() : 0;
     }
     if (st == SV_OK && !p->sched.end_phys.empty()) s->phys = p->sched.end_phys;  // layout-changing plan
@@ -658,6 +690,10 @@ sv_status sv_amplitudes(sv_state s, uint64_t first, uint64_t count, void* host_o
 sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_out) {
     if (!s || !host_out || (nq > 0 && !qubits)) return fail(SV_ERR_ARG, "NULL argument");
     if (nq < 0 || nq > s->n || nq > 28) return fail(SV_ERR_RANGE, "nq must be in [0, min(n, 28)]");
+    {
+        const sv_status st = materialize(s);
+        if (st != SV_OK) return st;
+    }
     for (int j = 0; j < nq; ++j) {
         if (qubits[j] < 0 || qubits[j] >= s->n) return fail(SV_ERR_RANGE, "qubit out of range");
         for (int i = 0; i < j; ++i)
@@ -776,6 +812,10 @@ sv_status sv_norm(sv_state s, double* out) {
 
 sv_status sv_sync(sv_state s) {
     if (!s) return fail(SV_ERR_ARG, "NULL state");
+    {
+        const sv_status st = materialize(s);
+        if (st != SV_OK) return st;
+    }
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
     return SV_OK;
@@ -792,6 +832,10 @@ sv_status sv_info(sv_state s, int* n, int* n_local, int* world, int* rank, sv_dt
 }
 
 sv_status sv_device_ptr(sv_state s, void** dev_ptr, uint64_t* local_amps) {
+    if (s) {
+        const sv_status st = materialize(s);
+        if (st != SV_OK) return st;
+    }
     if (!s) return fail(SV_ERR_ARG, "NULL state");
     if (dev_ptr) *dev_ptr = s->d;
     if (local_amps) *local_amps = s->virt ? (1ull << s->n) : s->local_amps();

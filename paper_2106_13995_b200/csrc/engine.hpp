@@ -103,6 +103,7 @@ struct PassPlan {
     double perm_cost = 1.0;              // PERM: estimated cost in HBM passes
     std::shared_ptr<TileSym> sym;        // TILE: the symbolic pass
     void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
+    void* jit_fn_basis = nullptr;        // TILE, first pass: variant whose input is a basis state
     int jit_threads = 0;
     size_t jit_smem = 0;
     bool jit_persistent = false;         // TILE: persistent grid (prefetching kernel)

@@ -655,7 +655,7 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 }  // namespace
 
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc) {
+                            int& tpc, bool basis_in) {
     Em e;
     e.dbl = sym.dbl;
     const int rb = sym.rb, R = 1 << rb;
@@ -663,7 +663,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     const int tb = m - rb;
     const int tthreads = 1 << tb;  // threads per tile
     const bool multi = sym.stages.size() > 1;
-    const bool pf = prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
+    const bool pf = !basis_in && prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
                     ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)tthreads == 0;
     persistent = pf;
     const size_t tile_bytes = ((size_t)1 << m) * (sym.dbl ? 16 : 8);
@@ -709,7 +709,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (pf)
         while (first + 1 < sym.stages.size() && sym.stages[first].ops.empty()) ++first;  // I/O-only stage
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
-      << (pf ? 1 : min_blocks(threads)) << ") svpass(C* __restrict__ psi){\n";
+      << (pf ? 1 : min_blocks(threads)) << ") svpass(C* __restrict__ psi"
+      << (basis_in ? ",unsigned long long kb" : "") << "){\n";
     if (pf) o << "extern __shared__ C sm[];\n";
     else if (multi && tpc > 1) o << "extern __shared__ C sm_[];\nC* sm=sm_+((threadIdx.x>>" << tb << ")<<" << m << ");\n";
     else if (multi) o << "extern __shared__ C sm[];\n";
@@ -811,7 +812,14 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             o << "{unsigned y=tl>>" << lb << ", f=0; while(y){f^=y&" << ((1u << lb) - 1) << "u; y>>=" << lb
               << ";} tl^=f&" << smask << "u;}\n";
         }
-        if (!reads_smem) {
+        if (!reads_smem && basis_in) {
+            // the pass input is the basis state |kb>: synthesise the tile, read nothing
+            const std::string one = sym.dbl ? "mk(1.0,0.0)" : "0x000000003f800000ull";
+            const std::string zero = sym.dbl ? "mk(0.0,0.0)" : "0ull";
+            for (int s = 0; s < R; ++s)
+                o << reg(s) << "=(kb==(g|" << goff[s] << "ull))?" << one << ":" << zero << ";";
+            o << "\n";
+        } else if (!reads_smem) {
             for (int s = 0; s < R; ++s) o << reg(s) << "=psi[g+" << goff[s] << "ull];";
             o << "\n";
         } else {
@@ -1014,12 +1022,17 @@ std::string gen_perm_source(const PassPlan& pp, bool dbl, int& threads) {
     return o.str();
 }
 
-sv_status jit_prepare(Schedule& sc, std::string& err) {
+sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
     std::vector<PassPlan*> todo;
     for (PassPlan& pp : sc.passes)
         if (((pp.kind == PassPlan::TILE && pp.sym) || pp.kind == PassPlan::PERM) && !pp.jit_fn) todo.push_back(&pp);
-    if (todo.empty()) return SV_OK;
-    std::vector<std::string> srcs(todo.size());
+    // the first pass, if a generated tile pass, also gets its basis-input variant (fused init)
+    PassPlan* first = (with_basis && !sc.passes.empty() && sc.passes[0].kind == PassPlan::TILE && sc.passes[0].sym &&
+                       !sc.passes[0].jit_fn_basis)
+                          ? &sc.passes[0]
+                          : nullptr;
+    if (todo.empty() && !first) return SV_OK;
+    std::vector<std::string> srcs(todo.size() + (first ? 1 : 0));
     for (size_t i = 0; i < todo.size(); ++i) {
         if (todo[i]->kind == PassPlan::PERM) {
             srcs[i] = gen_perm_source(*todo[i], todo[i]->perm_dbl, todo[i]->jit_threads);
@@ -1032,25 +1045,34 @@ sv_status jit_prepare(Schedule& sc, std::string& err) {
             todo[i]->jit_grid = (unsigned)(todo[i]->ntiles / (uint64_t)tpc);
         }
     }
-    std::vector<sv_status> st(todo.size(), SV_OK);
-    std::vector<std::string> errs(todo.size());
-    std::vector<void*> fns(todo.size(), nullptr);
+    size_t basis_smem = 0;
+    if (first) {
+        int th, tpc;
+        bool pers;
+        srcs.back() = gen_pass_source(*first->sym, first->ntiles, th, basis_smem, pers, tpc, true);
+    }
+    const size_t nsrc = srcs.size();
+    std::vector<sv_status> st(nsrc, SV_OK);
+    std::vector<std::string> errs(nsrc);
+    std::vector<void*> fns(nsrc, nullptr);
     int dev = 0;
     cudaGetDevice(&dev);
-    const size_t nthr = std::max<size_t>(1, std::min<size_t>(todo.size(), std::thread::hardware_concurrency()));
+    const size_t nthr = std::max<size_t>(1, std::min<size_t>(nsrc, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
     for (size_t w = 0; w < nthr; ++w)
         pool.emplace_back([&, w]() {
             cudaSetDevice(dev);
-            for (size_t i = w; i < todo.size(); i += nthr)
-                st[i] = jit_compile(srcs[i], todo[i]->jit_smem, &fns[i], errs[i]);
+            for (size_t i = w; i < nsrc; i += nthr)
+                st[i] = jit_compile(srcs[i], i < todo.size() ? todo[i]->jit_smem : basis_smem, &fns[i], errs[i]);
         });
     for (auto& th : pool) th.join();
-    for (size_t i = 0; i < todo.size(); ++i) {
+    for (size_t i = 0; i < nsrc; ++i)
         if (st[i] != SV_OK) {
             err = errs[i];
             return st[i];
         }
+    if (first) first->jit_fn_basis = fns.back();
+    for (size_t i = 0; i < todo.size(); ++i) {
         todo[i]->jit_fn = fns[i];
         if (todo[i]->jit_persistent) {
             int per_sm = 0, nsm = 148;
@@ -1068,6 +1090,13 @@ cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream) {
     void* args[] = {&psi};
     const unsigned grid = pp.jit_grid;
     return cudaLaunchKernel(pp.jit_fn, dim3(grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem, stream);
+}
+
+cudaError_t jit_launch_basis(const PassPlan& pp, void* psi, uint64_t kb, cudaStream_t stream) {
+    unsigned long long k = kb;
+    void* args[] = {&psi, &k};
+    return cudaLaunchKernel(pp.jit_fn_basis, dim3(pp.jit_grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem,
+                            stream);
 }
 
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {

@@ -578,6 +578,14 @@ double op_cost(const LOp& op) {
     }
 }
 
+double heavy_pass_cost() {
+    static double b = [] {
+        const char* e = getenv("SV_HEAVY_COST");
+        return e ? atof(e) : 200.0;
+    }();
+    return b;
+}
+
 bool diag_into_regs() {
     static bool b = [] {
         const char* e = getenv("SV_DIAG_REG");
@@ -715,6 +723,19 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             continue;
         }
         uint64_t S = select(remaining, lowmask, pass_ops, deferred, nullptr);
+        // Register bits of this pass: a heavy complex64 pass takes one fewer (half the code per
+        // op): its straight-line kernel otherwise outgrows the instruction cache and stalls on
+        // fetch (profiles/r01_icache.txt: 50% no_instructions at ~4000 instructions).
+        int rbp = rb;
+        if (o.use_jit() && !dbl && rb == 5) {
+            double cs = 0;
+            bool narrow = true;
+            for (int idx : pass_ops) {
+                cs += op_cost(ops[idx]);
+                narrow &= (int)ops[idx].tq.size() <= rb - 1;
+            }
+            if (narrow && cs > heavy_pass_cost()) rbp = rb - 1;
+        }
         // ---- cut the pass into register stages
         std::vector<StagePlan> stages;
         std::vector<int> todo(pass_ops.size());
@@ -736,7 +757,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                     const bool wide = (op.kind == OP_U3 || op.kind == OP_U4);
                     if (wide && !sp.wide.empty() && sp.wide != op.tq) { sdef.push_back(i); sblocked.add(op); continue; }
                     const uint64_t need = sp.R | qmask(op.tq);
-                    const bool fits = allowed ? ((qmask(op.tq) & ~allowed) == 0) : popc(need) <= rb;
+                    const bool fits = allowed ? ((qmask(op.tq) & ~allowed) == 0) : popc(need) <= rbp;
                     if (fits) {
                         sp.R = need;
                         sp.ops.push_back(i);
@@ -773,9 +794,9 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                 auto penalty = [&](uint64_t R) { return (stages.empty() && (R & lowq)) ? 3.0 : 0.0; };
                 double best = best_score - penalty(sp.R);
                 const int nq = (int)qs.size();
-                if (nq > rb && nq <= 16) {
+                if (nq > rbp && nq <= 16) {
                     // enumerate rb-subsets of qs (Gosper's hack)
-                    uint32_t c = (1u << rb) - 1;
+                    uint32_t c = (1u << rbp) - 1;
                     int evaluated = 0;
                     while (c < (1u << nq) && evaluated < 5000) {
                         uint64_t R = 0;
@@ -807,7 +828,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                     for (int q : op.dq) cnt[q] += 2;
                     for (int q : op.ctrl) cnt[q] += 1;
                 }
-                while (popc(sp.R) < rb) {
+                while (popc(sp.R) < rbp) {
                     int best = -1;
                     for (int q = 0; q < 64; ++q)
                         if (cnt[q] > 0 && !((sp.R >> q) & 1) && ((S >> q) & 1) && (best < 0 || cnt[q] > cnt[best]))
@@ -820,7 +841,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             todo = std::move(sdef);
         }
         // ---- tile qubits: pad to m_pad (threads) with the lowest free qubits
-        for (int q = 0; q < nl && popc(S) < std::max(m_pad, rb); ++q) S |= 1ull << q;
+        for (int q = 0; q < nl && popc(S) < std::max(m_pad, rbp); ++q) S |= 1ull << q;
         if (stages.size() > 1) {
             // multi-stage passes are bounded by shared memory (2^m amplitudes)
             for (int q = nl - 1; q >= 0 && popc(S) > m_max; --q) {
@@ -886,13 +907,15 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             for (int q = 0; q < 64; ++q) if ((S >> q) & 1) fprintf(stderr, "%d ", q);
             fprintf(stderr, "| low ->");
             for (int q : lowset) fprintf(stderr, " %d", q);
-            fprintf(stderr, " stages %zu\n", stages.size());
+            double cs = 0;
+            for (int idx : pass_ops) cs += op_cost(ops[idx]);
+            fprintf(stderr, " stages %zu cost %.1f\n", stages.size(), cs);
         }
         std::vector<const LOp*> pops;  // stage op indices refer to this list
         for (int idx : pass_ops) pops.push_back(&ops[idx]);
         PassPlan pp;
         pp.sym = std::make_shared<TileSym>();
-        if (!make_sym(pops, stages, S, rb, dbl, *pp.sym, err, perm.empty())) return SV_ERR_STATE;
+        if (!make_sym(pops, stages, S, rbp, dbl, *pp.sym, err, perm.empty())) return SV_ERR_STATE;
         if (!perm.empty()) {
             TileSym& sym = *pp.sym;
             // the qubits landing at the bottom must be the store's lanes, in output order
@@ -907,7 +930,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             // a single stage would load and store through the same lanes: split it
             if (sym.stages.size() == 1 || conflicts(sym.stages.back())) {
                 StageSym io;
-                for (int b = (int)sym.tq.size() - 1; b >= 0 && (int)io.rq.size() < rb; --b)
+                for (int b = (int)sym.tq.size() - 1; b >= 0 && (int)io.rq.size() < rbp; --b)
                     if (std::find(lanes.begin(), lanes.end(), sym.tq[b]) == lanes.end()) io.rq.push_back(sym.tq[b]);
                 sym.stages.push_back(io);
             }

@@ -31,6 +31,10 @@ struct sv_state_s {
     double* d_scratch = nullptr;
     size_t scratch_doubles = 0;
     int device = 0;
+    // Deferred basis-state initialisation (single GPU): the state is |lazy_basis> but not yet
+    // written; the first generated tile pass of the next plan synthesises its input tile instead
+    // of reading it (init fused into pass 0), anything else materialises it first.
+    int64_t lazy_basis = -1;
 
     size_t amp_bytes() const { return dbl ? 16 : 8; }
     uint64_t local_amps() const { return 1ull << nl; }

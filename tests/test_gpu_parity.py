@@ -247,6 +247,35 @@ def test_wide_marginals_relabelled_layout(P, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_fused_basis_init(P, dtype):
+    """sv_init_basis is deferred and synthesised by the plan's first pass: same result, bit
+    for bit, as the same plan run on the basis state written explicitly; readouts and
+    single gates after an init see the written state."""
+    n = 20
+    for c in (W.supremacy(5, 4, 10, seed=4), W.multiplier(5)):
+        text = W.to_text(c)
+        plan = P.Plan(text, dtype)
+        for k in (0, 1 << (c.n - 1), 0x5A5A5 & ((1 << c.n) - 1)):
+            e = np.zeros(1 << c.n, np.complex128)
+            e[k] = 1
+            with P.StateVector(c.n, dtype) as a, P.StateVector(c.n, dtype) as b:
+                a.init_basis(k)
+                a.apply_plan(plan)
+                b.set_amplitudes(e)
+                b.apply_plan(plan)
+                assert np.array_equal(a.amplitudes(), b.amplitudes()), (c.family, k)
+    with P.StateVector(n, dtype) as sv:
+        sv.init_basis(77)
+        assert sv.amplitudes(77, 1)[0] == 1 and sv.norm() == 1
+        sv.init_basis(5)
+        p = sv.probabilities([0, 2])
+        assert p[3] == 1
+        sv.init_basis(6)
+        sv.apply_gate(np.array([[0, 1], [1, 0]], complex), [0])
+        assert sv.amplitudes(7, 1)[0] == 1
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_init_states(P, dtype):
     for n in (1, 7, 20):
         with P.StateVector(n, dtype) as sv:

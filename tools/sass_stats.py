@@ -24,6 +24,8 @@ ap.add_argument("--tile", type=int, default=0)
 a = ap.parse_args()
 if a.workload == "supremacy":
     c = W.supremacy(6, 5, 20, 0) if a.qubits == 30 else W.supremacy((a.qubits + 4) // 5, 5, 20, 0, n=a.qubits)
+elif a.workload == "qft":
+    c = W.qft(a.qubits)
 else:
     c = W.multiplier(8, 7)
 plan = P.Plan(W.to_text(c), a.dtype, tile_qubits=a.tile)
@@ -50,8 +52,8 @@ with tempfile.TemporaryDirectory() as d:
         fp = sum(cnt[k] for k in ("FADD", "FFMA", "FMUL", "DADD", "DFMA", "DMUL", "FADD2", "FFMA2", "FMUL2"))
         R = 1 << rb
         # FP pipe cycles per warp on one SMSP (B200, tools/micro/fp_rate.cu): FADD2/FMUL2 2,
-        # FFMA2 3, scalar FP32 1, DADD/DMUL 2, DFMA 2.2
-        pipe = (2 * (cnt["FADD2"] + cnt["FMUL2"]) + 3 * cnt["FFMA2"] + cnt["FADD"] + cnt["FFMA"] + cnt["FMUL"]
+        # FFMA2 with an immediate 2 (3 with three register operands), scalar FP32 1, DADD/DMUL 2, DFMA 2.2
+        pipe = (2 * (cnt["FADD2"] + cnt["FMUL2"]) + 2 * cnt["FFMA2"] + cnt["FADD"] + cnt["FFMA"] + cnt["FMUL"]
                 + 2 * (cnt["DADD"] + cnt["DMUL"]) + 2.2 * cnt["DFMA"])
         tot.update(cnt)
         print(f"pass {i}: {hdr[24:]}, regs {regs.group(1) if regs else '?'}, instr/thread {n}, "
