@@ -709,7 +709,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (pf)
         while (first + 1 < sym.stages.size() && sym.stages[first].ops.empty()) ++first;  // I/O-only stage
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
-      << (pf ? 1 : min_blocks(threads)) << ") svpass(C* __restrict__ psi"
+      << (pf ? std::max(1, min_blocks(threads) / 2) : min_blocks(threads)) << ") svpass(C* __restrict__ psi"
       << (basis_in ? ",unsigned long long kb" : "") << "){\n";
     if (pf) o << "extern __shared__ C sm[];\n";
     else if (multi && tpc > 1) o << "extern __shared__ C sm_[];\nC* sm=sm_+((threadIdx.x>>" << tb << ")<<" << m << ");\n";
@@ -717,7 +717,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (tpc > 1) o << "const unsigned t=threadIdx.x&" << (tthreads - 1) << "u;\n";
     else o << "const unsigned t=threadIdx.x;\n";
     o << "C v[" << R << "];\nunsigned long long g,base;\n";
-    if (multi || pf) o << "unsigned tl;\n";
+    if (multi || pf) o << "unsigned tl,tr,tw;\n";
     const int L = sym.dbl ? 4 : 5;  // the tile's low qubits 0..L-1 are contiguous in memory
     if (pf) {
         const int E = sym.dbl ? 1 : 2;  // elements per 16-byte chunk
@@ -768,17 +768,19 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     PassState ps;
     ps.ph.assign(R, cd(1, 0));
     ps.rs.assign(R, std::string());
-    for (size_t si = first; si < sym.stages.size(); ++si) {
+    // thread-bit order of every stage: thread bit i <-> tile qubit tq_phys[i] (local position
+    // tq_local[i]); a stage's lane_first qubits take the lowest thread bits
+    const size_t NS = sym.stages.size();
+    std::vector<std::vector<int>> st_phys(NS), st_local(NS);
+    for (size_t si = 0; si < NS; ++si) {
         const StageSym& st = sym.stages[si];
-        StageCtx sc;
-        sc.rb = rb;
-        for (int i = 0; i < 64; ++i) sc.pos[i] = -1;
-        for (int j = 0; j < rb; ++j) sc.pos[st.rq[j]] = j;
         std::vector<int> tq_phys, tq_local;
         for (int b = 0; b < m; ++b)
-            if (sc.pos[sym.tq[b]] < 0) { tq_phys.push_back(sym.tq[b]); tq_local.push_back(b); }
+            if (std::find(st.rq.begin(), st.rq.end(), sym.tq[b]) == st.rq.end()) {
+                tq_phys.push_back(sym.tq[b]);
+                tq_local.push_back(b);
+            }
         if (!st.lane_first.empty()) {
-            // the stage's lowest thread bits take these qubits (the store's coalesced lanes)
             std::vector<int> p2, l2;
             for (int q : st.lane_first) { p2.push_back(q); l2.push_back(local_of[q]); }
             for (size_t i = 0; i < tq_phys.size(); ++i)
@@ -789,28 +791,114 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             tq_phys = p2;
             tq_local = l2;
         }
+        st_phys[si] = tq_phys;
+        st_local[si] = tq_local;
+    }
+    // Shared-memory layout of each stage transition k (stage k writes, k+1 reads): slot
+    // swz_k(x) = x ^ sum_{p >= lb, x_p = 1} a_k[p], a GF(2)-linear XOR into the low lb slot bits
+    // (lb = log2 of the slots per 128-byte wavefront phase).  a_k is chosen so that the lanes
+    // of one phase (thread bits 0..lb-1) hit distinct banks for BOTH the writer and the reader.
+    const int lbk = sym.dbl ? 3 : 4;
+    std::vector<std::vector<uint32_t>> swa(NS, std::vector<uint32_t>(m, 0));
+    for (size_t k = 0; k + 1 < NS; ++k) {
+        std::vector<uint32_t>& a = swa[k];
+        for (int p = lbk; p < m; ++p) a[p] = 1u << ((p - lbk) % lbk);
+        auto col = [&](int p) { return p < lbk ? (1u << p) : a[p]; };
+        auto full_rank = [&](const std::vector<int>& P) {
+            uint32_t basis[8] = {0};
+            int r = 0;
+            for (size_t i = 0; i < P.size() && (int)i < lbk; ++i) {
+                uint32_t v = col(P[i]);
+                for (int b = lbk - 1; b >= 0 && v; --b) {
+                    if (!((v >> b) & 1)) continue;
+                    if (!basis[b]) { basis[b] = v; ++r; v = 0; break; }
+                    v ^= basis[b];
+                }
+            }
+            return r == lbk;
+        };
+        std::vector<int> Pw(st_local[k].begin(), st_local[k].begin() + std::min<size_t>(lbk, st_local[k].size()));
+        std::vector<int> Pr(st_local[k + 1].begin(),
+                            st_local[k + 1].begin() + std::min<size_t>(lbk, st_local[k + 1].size()));
+        // measured (profiles/r01_swizzle.txt): a win for complex64 (27.35 vs 28.14 ms), a loss
+        // for complex128 (60.1 vs 58.7 ms, its heaviest pass slows down although its bank
+        // conflicts drop 250x), so complex128 keeps the fixed fold unless SV_SWZ_SEARCH=1
+        static const int search_env = [] {
+            const char* e = getenv("SV_SWZ_SEARCH");
+            return e ? atoi(e) : -1;
+        }();
+        const bool search = search_env < 0 ? !sym.dbl : search_env != 0;
+        if (!search || pf || (int)Pw.size() < lbk || (int)Pr.size() < lbk || (full_rank(Pw) && full_rank(Pr)))
+            continue;
+        std::vector<int> Q;
+        for (int p : Pw) if (p >= lbk) Q.push_back(p);
+        for (int p : Pr) if (p >= lbk && std::find(Q.begin(), Q.end(), p) == Q.end()) Q.push_back(p);
+        uint64_t rng = 0x9E3779B97F4A7C15ull ^ (k * 0x100000001B3ull);
+        const std::vector<uint32_t> a0 = a;
+        bool ok = false;
+        for (int tries = 0; tries < 20000 && !ok; ++tries) {
+            for (int p : Q) {
+                rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+                a[p] = 1u + (uint32_t)(rng % ((1u << lbk) - 1));
+            }
+            ok = full_rank(Pw) && full_rank(Pr);
+        }
+        if (!ok) a = a0;
+    }
+    auto swz_k = [&](size_t k, uint32_t x) {
+        if (pf) return swz_const(x, sym.dbl, pf);
+        uint32_t y = x;
+        for (int p = lbk; p < m; ++p)
+            if ((x >> p) & 1) y ^= swa[k][p];
+        return y;
+    };
+    // run-time slot of the thread part: tl ^ sum over thread bits i (local position >= lb) of a_k
+    auto swz_thread = [&](size_t k, const std::vector<int>& tq_local) {
+        std::ostringstream t;
+        t << "tl";
+        for (size_t i = 0; i < tq_local.size(); ++i)
+            if (tq_local[i] >= lbk && swa[k][tq_local[i]])
+                t << "^((0u-((t>>" << i << ")&1u))&" << swa[k][tq_local[i]] << "u)";
+        return t.str();
+    };
+    for (size_t si = first; si < sym.stages.size(); ++si) {
+        const StageSym& st = sym.stages[si];
+        StageCtx sc;
+        sc.rb = rb;
+        for (int i = 0; i < 64; ++i) sc.pos[i] = -1;
+        for (int j = 0; j < rb; ++j) sc.pos[st.rq[j]] = j;
+        const std::vector<int>& tq_phys = st_phys[si];
+        const std::vector<int>& tq_local = st_local[si];
         o << "// stage " << si << ": registers";
         for (int q : st.rq) o << " " << q;
         o << "\n";
         o << "g=base|" << deposit_expr(tq_phys, true) << ";\n";
         std::vector<uint64_t> goff(R);
-        std::vector<uint32_t> loff(R);
+        std::vector<uint32_t> loff(R), loffw(R);
+        const bool reads_smem = pf || si > first;
+        const bool writes_smem = si + 1 < sym.stages.size();
         for (int s = 0; s < R; ++s) {
             uint64_t go = 0;
             uint32_t lo = 0;
             for (int j = 0; j < rb; ++j)
                 if ((s >> j) & 1) { go |= 1ull << st.rq[j]; lo |= 1u << local_of[st.rq[j]]; }
             goff[s] = go;
-            loff[s] = swz_const(lo, sym.dbl, pf);
+            loff[s] = pf ? swz_const(lo, sym.dbl, pf) : (si > 0 ? swz_k(si - 1, lo) : 0);
+            loffw[s] = pf ? loff[s] : (writes_smem ? swz_k(si, lo) : 0);
         }
-        const bool reads_smem = pf || si > first;
-        const bool writes_smem = si + 1 < sym.stages.size();
         if (reads_smem || writes_smem) {
             const std::string tl = deposit_expr(tq_local, false);
-            const int lb = sym.dbl ? 3 : 4;
             o << "tl=" << tl << ";\n";
-            o << "{unsigned y=tl>>" << lb << ", f=0; while(y){f^=y&" << ((1u << lb) - 1) << "u; y>>=" << lb
-              << ";} tl^=f&" << smask << "u;}\n";
+            if (pf) {
+                const int lb = sym.dbl ? 3 : 4;
+                o << "{unsigned y=tl>>" << lb << ", f=0; while(y){f^=y&" << ((1u << lb) - 1) << "u; y>>=" << lb
+                  << ";} tl^=f&" << smask << "u;}\n";
+                o << "tr=tl; tw=tl;\n";
+            } else {
+                if (reads_smem) o << "tr=" << swz_thread(si - 1, tq_local) << ";";
+                if (writes_smem) o << "tw=" << swz_thread(si, tq_local) << ";";
+                o << "\n";
+            }
         }
         if (!reads_smem && basis_in) {
             // the pass input is the basis state |kb>: synthesise the tile, read nothing
@@ -824,7 +912,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             o << "\n";
         } else {
             if (si > first) o << "__syncthreads();\n";
-            for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[tl^" << loff[s] << "u];";
+            for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[tr^" << loff[s] << "u];";
             o << "\n";
         }
         for (const LOp& op : st.ops) emit_op(e, op, sc, ps);
@@ -881,7 +969,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         } else {
             // unit phases are tied to this stage's register numbering: apply before re-distribution
             for (int s = 0; s < R; ++s) flush_ph(e, ps, s);
-            for (int s = 0; s < R; ++s) o << SM << "[tl^" << loff[s] << "u]=" << reg(s) << ";";
+            for (int s = 0; s < R; ++s) o << SM << "[tw^" << loffw[s] << "u]=" << reg(s) << ";";
             o << "\n";
         }
     }
@@ -1046,6 +1134,10 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
         }
     }
     size_t basis_smem = 0;
+    if (first && first->jit_persistent) {  // persistent launch shape: no basis variant
+        first = nullptr;
+        srcs.pop_back();
+    }
     if (first) {
         int th, tpc;
         bool pers;
