@@ -820,14 +820,13 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         std::vector<int> Pw(st_local[k].begin(), st_local[k].begin() + std::min<size_t>(lbk, st_local[k].size()));
         std::vector<int> Pr(st_local[k + 1].begin(),
                             st_local[k + 1].begin() + std::min<size_t>(lbk, st_local[k + 1].size()));
-        // measured (profiles/r01_swizzle.txt): a win for complex64 (27.35 vs 28.14 ms), a loss
-        // for complex128 (60.1 vs 58.7 ms, its heaviest pass slows down although its bank
-        // conflicts drop 250x), so complex128 keeps the fixed fold unless SV_SWZ_SEARCH=1
-        static const int search_env = [] {
+        // measured (profiles/r01_swizzle.txt): complex64 27.35 vs 28.14 ms; complex128 57.4
+        // vs 58.7 ms once its heaviest pass runs with 3 register bits (with 4 that pass slowed
+        // down on instruction fetch when its bank conflicts went away)
+        static const bool search = [] {
             const char* e = getenv("SV_SWZ_SEARCH");
-            return e ? atoi(e) : -1;
+            return e ? atoi(e) != 0 : true;
         }();
-        const bool search = search_env < 0 ? !sym.dbl : search_env != 0;
         if (!search || pf || (int)Pw.size() < lbk || (int)Pr.size() < lbk || (full_rank(Pw) && full_rank(Pr)))
             continue;
         std::vector<int> Q;
@@ -969,6 +968,10 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         } else {
             // unit phases are tied to this stage's register numbering: apply before re-distribution
             for (int s = 0; s < R; ++s) flush_ph(e, ps, s);
+            // a stage that read the buffer in the previous transition's layout and writes it in
+            // a different one must wait for every thread's reads first (its slots are other
+            // threads' sources)
+            if (!pf && si > first && reads_smem && swa[si - 1] != swa[si]) o << "__syncthreads();\n";
             for (int s = 0; s < R; ++s) o << SM << "[tw^" << loffw[s] << "u]=" << reg(s) << ";";
             o << "\n";
         }

@@ -578,12 +578,16 @@ double op_cost(const LOp& op) {
     }
 }
 
-double heavy_pass_cost() {
+double heavy_pass_cost(bool dbl) {
     static double b = [] {
         const char* e = getenv("SV_HEAVY_COST");
         return e ? atof(e) : 200.0;
     }();
-    return b;
+    static double b2 = [] {
+        const char* e = getenv("SV_HEAVY_COST128");
+        return e ? atof(e) : 200.0;
+    }();
+    return dbl ? b2 : b;
 }
 
 bool diag_into_regs() {
@@ -723,18 +727,18 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             continue;
         }
         uint64_t S = select(remaining, lowmask, pass_ops, deferred, nullptr);
-        // Register bits of this pass: a heavy complex64 pass takes one fewer (half the code per
-        // op): its straight-line kernel otherwise outgrows the instruction cache and stalls on
-        // fetch (profiles/r01_icache.txt: 50% no_instructions at ~4000 instructions).
+        // Register bits of this pass: a heavy pass takes one fewer (half the code per op): its
+        // straight-line kernel otherwise outgrows the instruction cache and stalls on fetch
+        // (profiles/r01_icache.txt: 50% no_instructions at ~4000 instructions).
         int rbp = rb;
-        if (o.use_jit() && !dbl && rb == 5) {
+        if (o.use_jit() && ((!dbl && rb == 5) || (dbl && rb == 4))) {
             double cs = 0;
             bool narrow = true;
             for (int idx : pass_ops) {
                 cs += op_cost(ops[idx]);
                 narrow &= (int)ops[idx].tq.size() <= rb - 1;
             }
-            if (narrow && cs > heavy_pass_cost()) rbp = rb - 1;
+            if (narrow && cs > heavy_pass_cost(dbl)) rbp = rb - 1;
         }
         // ---- cut the pass into register stages
         std::vector<StagePlan> stages;
