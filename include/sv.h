@@ -134,7 +134,9 @@ sv_status sv_init_uniform(sv_state s);                  /* every amplitude 2^(-n
 sv_status sv_set_amplitudes(sv_state s, uint64_t first, uint64_t count, const void* host);
 
 /* Apply one gate.  mat: 2^k x 2^k complex matrix, row-major, interleaved
- * (re, im) doubles, rounded to the state dtype before use and copied before return.
+ * (re, im) doubles, rounded to the state dtype before use and copied before return; an
+ * entry component within 2^-52 of 0, +1 or -1 is taken as exactly that value (as in the IR's
+ * custom matrices), e.g. cos(pi/2) = 6.1e-17.
  * 1 <= k <= 5; targets[k]; controls[ncontrols] (may be NULL when ncontrols == 0).
  * SV_ERR_RANGE on qubit >= n or duplicates across targets and controls. */
 sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets,

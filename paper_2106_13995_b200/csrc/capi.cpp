@@ -455,7 +455,7 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
     }
     const size_t d = (size_t)1 << k;
     g.U.resize(d * d);
-    for (size_t i = 0; i < d * d; ++i) g.U[i] = cd(mat[2 * i], mat[2 * i + 1]);
+    for (size_t i = 0; i < d * d; ++i) g.U[i] = cd(snap_entry(mat[2 * i]), snap_entry(mat[2 * i + 1]));
     sv_plan_s plan;
     plan.circ.n = s->n;
     plan.circ.gates.push_back(std::move(g));

@@ -69,6 +69,17 @@ struct RunOpts {
 
 // Lower one gate to ops on physical local qubits; folds global qubits (rank constants).
 // needs_global: set when a non-diagonal target is global (caller must swap first).
+// A matrix entry component within 2^-52 of 0, +1 or -1 is taken as exact (cos(pi/2) =
+// 6.1e-17 in a user's CPhase(pi/2) is the exact 0 it stands for, below fp64 rounding of the
+// entry): the classifier then sees the unit phase and folds it for free.
+inline double snap_entry(double x) {
+    const double e = 2.220446049250313e-16;
+    if (x > -e && x < e) return 0.0;
+    if (x > 1.0 - e && x < 1.0 + e) return 1.0;
+    if (x > -1.0 - e && x < -1.0 + e) return -1.0;
+    return x;
+}
+
 sv_status lower_gate(const Gate& g, int gi, const Context& ctx, const RunOpts& o, std::vector<LOp>& out,
                      bool& needs_global, std::string& err);
 

@@ -105,7 +105,7 @@ static sv_status parse_gate(const std::string& src, int n, int line, Gate& g, st
         }
         if (nums.size() != 2 * d * d) return fail(name + " matrix has the wrong size");
         g.U.resize(d * d);
-        for (size_t j = 0; j < d * d; ++j) g.U[j] = cd(nums[2 * j], nums[2 * j + 1]);
+        for (size_t j = 0; j < d * d; ++j) g.U[j] = cd(snap_entry(nums[2 * j]), snap_entry(nums[2 * j + 1]));
     } else {
         int nc, k;
         std::vector<cd> U;

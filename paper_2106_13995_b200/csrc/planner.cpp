@@ -874,6 +874,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                 select(next, low, pn, dn, nullptr);
                 double sc = 0;
                 for (int i : pn) sc += op_cost(ops[i]);
+                if (dn.empty()) sc += 1e6;  // the next pass finishes the circuit
                 return sc + 1e-6 * popc(low & lowmask);
             };
             if (nt <= 20) {
