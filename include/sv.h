@@ -153,6 +153,9 @@ sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uin
  * Returns SV_ERR_RANGE for a bad pass index; an empty string for a non-tile pass. */
 sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len);
 sv_status sv_plan_destroy(sv_plan p);
+/* Logical -> physical qubit map the single-GPU schedule leaves (a relabelling schedule stores
+ * its final tiles permuted; readouts undo it).  phys_out: n ints, caller-owned. */
+sv_status sv_plan_qubit_map(sv_plan p, int* phys_out);
 
 /* Host-only dry run of the sharded schedule of a plan over `world` GPUs (power of two >= 2),
  * starting from the identity qubit map: number of global<->local exchange steps, of pass

@@ -60,6 +60,7 @@ def _load():
         "sv_apply_gate": (i, [vp, dp, i, ip, ip, i]),
         "sv_plan_compile": (i, [cp, i, ctypes.POINTER(RunOpts), ctypes.POINTER(vp)]),
         "sv_plan_info": (i, [vp, ip, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+        "sv_plan_qubit_map": (i, [vp, ip]),
         "sv_plan_destroy": (i, [vp]),
         "sv_plan_source": (i, [vp, i, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "sv_plan_apply": (i, [vp, vp, ctypes.POINTER(RunStats)]),
@@ -87,7 +88,7 @@ def _load():
 lib = _load()
 EXPORTED = ["sv_memory_estimate", "sv_create", "sv_wrap", "sv_nccl_unique_id", "sv_create_sharded",
             "sv_create_virtual_sharded", "sv_destroy", "sv_init_zero", "sv_init_basis", "sv_init_uniform",
-            "sv_set_amplitudes", "sv_apply_gate", "sv_plan_compile", "sv_plan_info", "sv_plan_source",
+            "sv_set_amplitudes", "sv_apply_gate", "sv_plan_compile", "sv_plan_info", "sv_plan_qubit_map", "sv_plan_source",
             "sv_plan_destroy", "sv_plan_pass_times", "sv_plan_shard_info",
             "sv_plan_apply", "sv_apply_circuit", "sv_amplitudes", "sv_probabilities", "sv_norm", "sv_sync",
             "sv_info", "sv_device_ptr", "sv_stream", "sv_qubit_map", "sv_last_error", "sv_version"]

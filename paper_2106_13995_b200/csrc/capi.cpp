@@ -496,6 +496,17 @@ sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uin
     return SV_OK;
 }
 
+sv_status sv_plan_qubit_map(sv_plan p, int* phys_out) {
+    if (!p || !phys_out) return fail(SV_ERR_ARG, "NULL argument");
+    if (!p->cached) {
+        const sv_status st = plan_schedule(p);
+        if (st != SV_OK) return st;
+    }
+    for (int q = 0; q < p->circ.n; ++q)
+        phys_out[q] = p->sched.end_phys.empty() ? q : p->sched.end_phys[q];
+    return SV_OK;
+}
+
 sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len) {
     if (!p) return fail(SV_ERR_ARG, "NULL plan");
     if (!p->cached || pass < 0 || pass >= (int)p->sched.passes.size()) return fail(SV_ERR_RANGE, "bad pass index");

@@ -186,13 +186,26 @@ using Pend = std::map<int, std::pair<cd, cd>>;
 //           matrix, or an operand modifier of the packed FP32 instruction), so those diagonal
 //           gates cost no instruction at all.
 //   rs   -- per-register pending run-time sign (name of a per-thread +-1 pair, packed backend)
+//   poly -- pending diagonal phase polynomial exp(i sum theta_ab x_a x_b) over physical qubits
+//           (a == b: a linear term): general phases and controlled phases (CPhase, QFT) are
+//           only summed here; the terms on a qubit are multiplied in once, when a
+//           non-diagonal op targets that qubit, or at the end of the pass.
 struct PassState {
     cd fac = 1;
     Pend pend;
     std::vector<cd> ph;
     std::vector<std::string> rs;
     std::map<std::string, std::string> sgprod;  // products of run-time signs already declared
+    std::map<std::pair<int, int>, double> poly;
 };
+
+bool phase_poly_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_PHASE_POLY");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
 
 bool is_unit(const cd& c) {
     return c == cd(1, 0) || c == cd(-1, 0) || c == cd(0, 1) || c == cd(0, -1);
@@ -363,6 +376,99 @@ void emit_flush(Em& e, const StageCtx& sc, PassState& ps, int q) {
     }
 }
 
+// run-time complex factor of a thread: product over (bit, theta) of (bit ? e^{i theta} : 1)
+std::string poly_runtime(Em& e, const std::vector<std::pair<std::vector<int>, double>>& f) {
+    std::string acc;
+    for (const auto& t : f) {
+        std::string cond;
+        for (int b : t.first) cond += (cond.empty() ? "" : "&&") + std::string("((g>>") + std::to_string(b) + ")&1ull)";
+        const cd c = std::polar(1.0, t.second);
+        const std::string name = "pz" + std::to_string(e.nvar++);
+        if (e.dbl) e.o << "const C " << name << "=(" << cond << ")?mk(" << e.lit(c.real()) << "," << e.lit(c.imag())
+                       << "):mk(1.0,0.0);";
+        else e.o << "const C " << name << "=(" << cond << ")?" << k2(c.real(), c.imag()) << ":0x000000003f800000ull;";
+        if (acc.empty()) {
+            acc = name;
+        } else {
+            const std::string prod = "pz" + std::to_string(e.nvar++);
+            e.o << "const C " << prod << "=CM(" << acc << "," << name << ");";
+            acc = prod;
+        }
+    }
+    return acc;
+}
+
+// v = v * (run-time k) * (compile-time c)
+void mul_runtime(Em& e, int s, const std::string& k, const cd& c, std::map<std::string, std::string>& cache) {
+    std::string kk = k;
+    if (!is1(c)) {
+        const std::string key = k + "|" + (e.dbl ? e.lit(c.real()) + "," + e.lit(c.imag()) : k2(c.real(), c.imag()));
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            const std::string name = "pk" + std::to_string(e.nvar++);
+            if (e.dbl) e.o << "const C " << name << "=CM(" << k << ",mk(" << e.lit(c.real()) << "," << e.lit(c.imag()) << "));";
+            else e.o << "const C " << name << "=CM(" << k << "," << k2(c.real(), c.imag()) << ");";
+            it = cache.emplace(key, name).first;
+        }
+        kk = it->second;
+    }
+    if (e.dbl) {
+        e.o << reg(s) << "=CM(" << reg(s) << "," << kk << ");";
+    } else {
+        const std::string key = "split|" + kk;
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            const std::string name = "ps" + std::to_string(e.nvar++);
+            e.o << "const C " << name << "r=pk(lo(" << kk << "),lo(" << kk << "))," << name << "i=pk(hi(" << kk << "),hi(" << kk
+                << "));";
+            it = cache.emplace(key, name).first;
+        }
+        e.o << reg(s) << "=F(I(" << reg(s) << ")," << it->second << "i,M(" << reg(s) << "," << it->second << "r));";
+    }
+}
+
+// multiply in the pending phase terms that involve physical qubit q (a register qubit here;
+// otherwise the terms stay pending)
+void poly_flush(Em& e, const StageCtx& sc, PassState& ps, int q) {
+    const int pq = sc.pos[q];
+    if (pq < 0) return;
+    double lin = 0;
+    std::vector<std::pair<int, double>> reg_terms;                  // (register position, theta)
+    std::vector<std::pair<std::vector<int>, double>> rt_terms;       // (thread/base qubits, theta)
+    bool any = false;
+    for (auto it = ps.poly.begin(); it != ps.poly.end();) {
+        const int a = it->first.first, b = it->first.second;
+        if (a != q && b != q) { ++it; continue; }
+        any = true;
+        const int o = a == q ? b : a;
+        if (o == q) lin += it->second;
+        else if (sc.pos[o] >= 0) reg_terms.push_back({sc.pos[o], it->second});
+        else rt_terms.push_back({{o}, it->second});
+        it = ps.poly.erase(it);
+    }
+    if (!any) return;
+    const int R = 1 << sc.rb;
+    const std::string rt = poly_runtime(e, rt_terms);
+    std::map<std::string, std::string> cache;
+    for (int s = 0; s < R; ++s) {
+        if (!((s >> pq) & 1)) continue;
+        double th = lin;
+        for (const auto& t : reg_terms)
+            if ((s >> t.first) & 1) th += t.second;
+        const cd c = std::polar(1.0, th);
+        if (rt.empty()) {
+            if (is_unit(c) || is1(c)) {
+                ps.ph[s] *= c;  // +-1, +-i: folded into the next reader
+                continue;
+            }
+            e.o << reg(s) << "=" << scaled(e, reg(s), c) << ";";
+        } else {
+            mul_runtime(e, s, rt, c, cache);
+        }
+    }
+    e.o << "\n";
+}
+
 void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
     const int R = 1 << sc.rb;
     cd& fac = ps.fac;
@@ -401,6 +507,20 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
             return;
         }
     }
+    // a general phase (optionally with one control): a phase-polynomial term, no code now
+    if (phase_poly_enabled() && k == 0 && op.dq.size() == 1 && op.ctrl.size() <= 1 &&
+        (op.kind == OP_PHASE || (op.kind == OP_DIAG1 && op.ctrl.empty()))) {
+        const cd c0 = op.kind == OP_DIAG1 ? op.coef[0] : cd(1, 0);
+        const cd c1 = op.kind == OP_DIAG1 ? op.coef[1] : op.coef[0];
+        if (std::abs(std::abs(c0) - 1) < 1e-12 && std::abs(std::abs(c1) - 1) < 1e-12 && !is_unit(c1 / c0)) {
+            ps.fac *= c0;
+            const int a = op.dq[0], b = op.ctrl.empty() ? a : op.ctrl[0];
+            ps.poly[{std::min(a, b), std::max(a, b)}] += std::arg(c1 / c0);
+            return;
+        }
+    }
+    if (k > 0)
+        for (int q : op.tq) poly_flush(e, sc, ps, q);
     // pending factors on the targets of a non-diagonal op
     if (k > 0) {
         if (controlled) {
@@ -684,6 +804,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         o << "typedef double R;\n";
         o << "struct alignas(16) C { R x, y; };\n";
         o << "__device__ __forceinline__ C mk(R x, R y){C c; c.x=x; c.y=y; return c;}\n";
+        o << "__device__ __forceinline__ C CM(C a, C b){return mk(a.x*b.x-a.y*b.y, a.x*b.y+a.y*b.x);}\n";
     } else {
         // packed complex64: lo = re, hi = im; paired FP32 ops (sm_100)
         o << "typedef unsigned long long C;\n"
@@ -697,7 +818,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
              "DI C F1(C a,C b,C c){return pk(fmaf(lo(a),lo(b),lo(c)),fmaf(hi(a),hi(b),hi(c)));}\n"
              "DI C N(C a){return pk(-lo(a),-hi(a));}\n"
              "DI C I(C a){return pk(-hi(a),lo(a));}\n"
-             "DI C NI(C a){return pk(hi(a),-lo(a));}\n";
+             "DI C NI(C a){return pk(hi(a),-lo(a));}\n"
+             "DI C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}\n";
         // FFMA2 issues at 1/3 per cycle on B200, two scalar FFMAs at 1 each
         // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes
         o << (scalar_fma() ? "#define F F1\n" : "#define F F2\n");
@@ -916,6 +1038,31 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         }
         for (const LOp& op : st.ops) emit_op(e, op, sc, ps);
         if (si + 1 == sym.stages.size()) {
+            // pending phase terms: by register qubit, then the thread/tile-base-only rest
+            for (bool again = true; again;) {
+                again = false;
+                for (const auto& kv : ps.poly) {
+                    const int r = sc.pos[kv.first.first] >= 0 ? kv.first.first
+                                  : sc.pos[kv.first.second] >= 0 ? kv.first.second : -1;
+                    if (r >= 0) {
+                        poly_flush(e, sc, ps, r);
+                        again = true;
+                        break;
+                    }
+                }
+            }
+            if (!ps.poly.empty()) {  // terms on thread / tile-base qubits only
+                std::vector<std::pair<std::vector<int>, double>> rest;
+                for (const auto& kv : ps.poly)
+                    rest.push_back({kv.first.first == kv.first.second ? std::vector<int>{kv.first.first}
+                                                                        : std::vector<int>{kv.first.first, kv.first.second},
+                                    kv.second});
+                ps.poly.clear();
+                const std::string G = poly_runtime(e, rest);
+                std::map<std::string, std::string> cache;
+                for (int s = 0; s < R; ++s) mul_runtime(e, s, G, 1, cache);
+                o << "\n";
+            }
             // pending factors of non-register qubits need the index bit: apply them first
             // (real ones join one per-thread scale, multiplied in with the deferred factor)
             std::vector<int> rt;

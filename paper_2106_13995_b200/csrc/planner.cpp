@@ -572,7 +572,7 @@ double op_cost(const LOp& op) {
         case OP_U4: return 64;
         case OP_T: case OP_TDG: return 1.3;
         case OP_Z: case OP_S: case OP_SDG: return 0.6;
-        case OP_PHASE: return 2;
+        case OP_PHASE: return 0.4;  // summed into the pass's phase polynomial (jit.cpp)
         case OP_DIAG1: case OP_DIAG2: case OP_SCALAR: return 4;
         default: return 1;
     }

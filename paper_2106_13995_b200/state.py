@@ -56,6 +56,13 @@ class Plan:
         check(lib.sv_plan_info(self._h, ctypes.byref(n), ctypes.byref(g), ctypes.byref(p), ctypes.byref(s)))
         return {"n": n.value, "gates": g.value, "passes": p.value, "stages": s.value}
 
+    def qubit_map(self):
+        """Logical -> physical qubit map the single-GPU schedule leaves behind."""
+        n = self.info()["n"]
+        out = (ctypes.c_int * n)()
+        check(lib.sv_plan_qubit_map(self._h, out))
+        return list(out)
+
     def shard_info(self, world: int) -> dict:
         """Host-only dry run of the sharded schedule over `world` GPUs (no GPU needed)."""
         s, b, p = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()

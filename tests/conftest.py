@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs the C-ABI path")
     config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "cpu_emulation: generated kernels executed on the host (tools/emulate.py)")
 
 
 def _has_cuda():

@@ -1,0 +1,92 @@
+"""The generated sm_100a pass kernels, executed on the host (tools/emulate.py: the CUDA source
+translated to C++, one std::thread per CUDA thread, a std::barrier per __syncthreads), against
+the oracle.  Covers the code generator without a GPU: relabelling stores, per-transition
+swizzles, deferred factors, run-time signs, the phase polynomial, both dtypes.  The GPU tests
+(tests/test_gpu_parity.py) run the same kernels on the B200."""
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import assert_close
+from tools.emulate import run_plan_on_host, to_logical
+
+pytestmark = pytest.mark.cpu_emulation
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2106_13995_b200 as P
+    return P
+
+
+def phase_heavy_circuit(n, ngates, seed):
+    from tests.test_gpu_parity import phase_heavy_circuit as f
+    return f(n, ngates, seed)
+
+
+def _emulated(P, text, n, dtype, psi):
+    plan = P.Plan(text, dtype)
+    x = psi.astype(np.complex64 if dtype == "c64" else np.complex128)
+    return run_plan_on_host(plan, x), plan
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_supremacy_14q(P, dtype):
+    c = W.supremacy(4, 4, 12, seed=2, n=14)
+    text = W.to_text(c)
+    psi = W.random_state(14, 3)
+    psi = W.round_to_c64(psi) if dtype == "c64" else psi
+    got, plan = _emulated(P, text, 14, dtype, psi)
+    assert plan.info()["passes"] >= 2
+    assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n,seed", [(6, 0), (14, 1)])
+def test_phase_polynomial(P, dtype, n, seed):
+    c = phase_heavy_circuit(n, 200, seed)
+    text = W.to_text(c)
+    psi = W.random_state(n, seed + 10)
+    psi = W.round_to_c64(psi) if dtype == "c64" else psi
+    got, _ = _emulated(P, text, n, dtype, psi)
+    assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))
+
+
+def test_qft_closed_form(P):
+    n, k = 13, 4321
+    c = W.concat(W.basis_prep(W.Circuit(n, []), k), W.qft(n))
+    psi = np.zeros(1 << n, complex)
+    psi[0] = 1
+    got, _ = _emulated(P, W.to_text(c), n, "c128", psi)
+    j = np.arange(1 << n)
+    assert np.max(np.abs(got - np.exp(2j * np.pi * j * k / (1 << n)) / np.sqrt(1 << n))) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_circuits(P, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(9, 14))
+    c = W.random_circuit(n, 60, seed, max_k=4, max_controls=2)
+    text = W.to_text(c)
+    psi = W.random_state(n, seed)
+    plan = P.Plan(text, "c128")
+    srcs = [plan.source(i) for i in range(plan.info()["passes"])]
+    if not all(srcs):
+        pytest.skip("plan has a non-tile pass")
+    got = run_plan_on_host(plan, psi)
+    assert_close(got, oracle.simulate(text, psi), "c128", W.gate_count(c))
+
+
+def test_to_logical_roundtrip():
+    n = 5
+    qmap = [3, 0, 4, 1, 2]
+    x = np.arange(1 << n) + 0j
+    # physical index of logical i
+    phys = np.zeros(1 << n, np.int64)
+    for i in range(1 << n):
+        phys[i] = sum(((i >> q) & 1) << qmap[q] for q in range(n))
+    y = np.zeros_like(x)
+    y[phys] = x
+    assert np.array_equal(to_logical(y, qmap, n), x)

@@ -126,6 +126,64 @@ def test_qft_closed_form_gpu(P):
     assert np.max(np.abs(got - expect)) <= 1e-12
 
 
+def phase_heavy_circuit(n, ngates, seed):
+    """Controlled phases (QFT-style), single-qubit diagonals with a global part, controlled
+    1-qubit phases, interleaved with H, SqrtX, X, SWAP, CNOT and dense 2-qubit U: every kind
+    of term of the generator's pending phase polynomial, with register, thread and tile-base
+    partners."""
+    rng = np.random.default_rng(seed)
+    gates = []
+    for _ in range(ngates):
+        r = rng.random()
+        th = float(rng.uniform(0, 2 * np.pi))
+        if r < 0.35:
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            m = np.diag([1, 1, 1, np.exp(1j * th)])
+            gates.append(W.GateSpec("U", (a, b), (), tuple(complex(x) for x in m.reshape(-1))))
+        elif r < 0.5:
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            m = np.diag([1, np.exp(1j * th)])
+            gates.append(W.GateSpec("CU", (a,), (b,), tuple(complex(x) for x in m.reshape(-1))))
+        elif r < 0.6:
+            a = int(rng.integers(n))
+            m = np.diag([np.exp(1j * th), np.exp(1j * float(rng.uniform(0, 2 * np.pi)))])
+            gates.append(W.GateSpec("U", (a,), (), tuple(complex(x) for x in m.reshape(-1))))
+        elif r < 0.9:
+            name = ["H", "SqrtX", "X", "H", "T"][int(rng.integers(5))]
+            gates.append(W.GateSpec(name, (int(rng.integers(n)),)))
+        elif r < 0.95:
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            gates.append(W.GateSpec(["SWAP", "CNOT"][int(rng.integers(2))], (a, b)))
+        else:
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            m = W.random_unitary(2, rng)
+            gates.append(W.GateSpec("U", (a, b), (), tuple(complex(x) for x in m.reshape(-1))))
+    return W.Circuit(n, [[g] for g in gates], "custom", {"seed": seed})
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n,seed", [(6, 0), (14, 1), (17, 2), (20, 3)])
+def test_phase_polynomial_circuits(P, dtype, n, seed):
+    c = phase_heavy_circuit(n, 300, seed)
+    text = W.to_text(c)
+    psi0 = input_for(n, seed + 10, dtype)
+    ref = oracle.simulate(text, psi0)
+    for mode in ({}, {"fuse": False}):
+        got, _ = run_gpu(P, text, n, dtype, psi0=psi0, **mode)
+        assert_close(got, ref, dtype, W.gate_count(c))
+
+
+def test_qft_20q_vs_oracle(P):
+    c = W.qft(20)
+    text = W.to_text(c)
+    psi0 = input_for(20, 4, "c128")
+    ref = oracle.simulate(text, psi0)
+    for dtype in ("c128", "c64"):
+        got, st = run_gpu(P, text, 20, dtype, psi0=input_for(20, 4, dtype))
+        assert_close(got, oracle.simulate(text, input_for(20, 4, dtype)) if dtype == "c64" else ref, dtype,
+                     W.gate_count(c))
+
+
 # ------------------------------------------------------------------ config 2: multiplier, basis inputs
 def test_config2_multiplier_21q_bit_exact(P):
     c = W.multiplier(5)

@@ -28,5 +28,6 @@ from .circuits import (  # noqa: F401
     remove_random_qubit,
     width_sweep,
     family_at_width,
+    random_unitary,
 )
 from .states import random_state, round_to_c64  # noqa: F401
