@@ -519,6 +519,20 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
             return;
         }
     }
+    // a general two-qubit diagonal of unit entries: c00 * exp(i(ta x_a + tb x_b + tab x_a x_b))
+    if (phase_poly_enabled() && k == 0 && op.kind == OP_DIAG2 && op.ctrl.empty()) {
+        const cd c00 = op.coef[0], c10 = op.coef[1], c01 = op.coef[2], c11 = op.coef[3];
+        bool unit = true;
+        for (const cd& c : op.coef) unit &= std::abs(std::abs(c) - 1) < 1e-12;
+        if (unit) {
+            const int a = op.dq[0], b = op.dq[1];
+            ps.fac *= c00;
+            ps.poly[{a, a}] += std::arg(c10 / c00);
+            ps.poly[{b, b}] += std::arg(c01 / c00);
+            ps.poly[{std::min(a, b), std::max(a, b)}] += std::arg(c11 * c00 / (c10 * c01));
+            return;
+        }
+    }
     if (k > 0)
         for (int q : op.tq) poly_flush(e, sc, ps, q);
     // pending factors on the targets of a non-diagonal op

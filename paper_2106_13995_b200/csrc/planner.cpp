@@ -573,7 +573,8 @@ double op_cost(const LOp& op) {
         case OP_T: case OP_TDG: return 1.3;
         case OP_Z: case OP_S: case OP_SDG: return 0.6;
         case OP_PHASE: return 0.4;  // summed into the pass's phase polynomial (jit.cpp)
-        case OP_DIAG1: case OP_DIAG2: case OP_SCALAR: return 4;
+        case OP_DIAG1: case OP_DIAG2: return 0.5;  // phase polynomial (jit.cpp)
+        case OP_SCALAR: return 0.2;
         default: return 1;
     }
 }

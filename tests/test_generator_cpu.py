@@ -64,6 +64,18 @@ def test_qft_closed_form(P):
     assert np.max(np.abs(got - np.exp(2j * np.pi * j * k / (1 << n)) / np.sqrt(1 << n))) <= 1e-12
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_diagonal_heavy(P, dtype):
+    """General 1- and 2-qubit diagonals (phase-polynomial terms incl. their global part)."""
+    n = 13
+    c = W.random_circuit(n, 80, 7, kinds=["Udiag", "H", "SqrtX", "CNOT", "T", "CZ"], max_k=2, max_controls=1)
+    text = W.to_text(c)
+    psi = W.random_state(n, 7)
+    psi = W.round_to_c64(psi) if dtype == "c64" else psi
+    got, _ = _emulated(P, text, n, dtype, psi)
+    assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_random_circuits(P, seed):
     rng = np.random.default_rng(seed)
