@@ -77,6 +77,11 @@ typedef struct {
     int check_unitary;   /* 1 = reject matrices with |U^dagger U - I| > 1e-9 */
     int use_graph;       /* 1 = record the plan's launches into a CUDA graph on first use */
     int profile;         /* 1 = bracket every pass with CUDA events (sv_plan_pass_times) */
+    int exchange;        /* sharded global<->local swaps: 0 (default) = fused into the preceding
+                            pass, whose stores go straight to the peers' second buffers over
+                            NVLink peer memory (CUDA IPC; needs a second shard
+                            buffer, falls back to 1 if it cannot be allocated or mapped on every
+                            rank); 1 = NCCL send/recv through a staging chunk */
 } sv_run_opts;
 
 typedef struct {

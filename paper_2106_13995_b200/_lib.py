@@ -25,7 +25,7 @@ class SvError(RuntimeError):
 class RunOpts(ctypes.Structure):
     _fields_ = [("fuse", ctypes.c_int), ("tile_qubits", ctypes.c_int), ("max_fused_k", ctypes.c_int),
                 ("force_kernel", ctypes.c_int), ("check_unitary", ctypes.c_int), ("use_graph", ctypes.c_int),
-                ("profile", ctypes.c_int)]
+                ("profile", ctypes.c_int), ("exchange", ctypes.c_int)]
 
 
 class RunStats(ctypes.Structure):

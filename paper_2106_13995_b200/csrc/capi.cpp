@@ -60,6 +60,7 @@ RunOpts to_opts(const sv_run_opts* o) {
         r.check_unitary = o->check_unitary != 0;
         r.use_graph = o->use_graph != 0;
         r.profile = o->profile != 0;
+        r.exchange = o->exchange;
     }
     return r;
 }
@@ -113,6 +114,8 @@ sv_status new_state(int n, int nl, int world, int rank, sv_dtype dt, void* strea
 
 void free_state(sv_state_s* s) {
     if (!s) return;
+    for (void* q : s->ipc_open) cudaIpcCloseMemHandle(q);
+    if (s->xflag) cudaFree(s->xflag);
     if (s->owned && s->d) cudaFree(s->d);
     if (s->d2) cudaFree(s->d2);
     if (s->d_scratch) cudaFree(s->d_scratch);
@@ -467,7 +470,8 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
 sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts* opts, sv_plan* out) {
     if (!out || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
     if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
-    if (opts && (opts->force_kernel < 0 || opts->force_kernel > 3 || opts->tile_qubits < 0))
+    if (opts && (opts->force_kernel < 0 || opts->force_kernel > 3 || opts->tile_qubits < 0 || opts->exchange < 0 ||
+                 opts->exchange > 1))
         return fail(SV_ERR_ARG, "bad sv_run_opts");
     auto* p = new sv_plan_s();
     std::string err;

@@ -69,4 +69,32 @@ sv_status comm_allgather_doubles(sv_state_s* s, const double* local, size_t coun
     return SV_OK;
 }
 
+sv_status comm_allgather_bytes(sv_state_s* s, const void* local, size_t bytes, std::vector<unsigned char>& all,
+                               std::string& err) {
+    unsigned char* d = nullptr;
+    if (cudaMalloc(&d, bytes * (s->world + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        err = "cudaMalloc for the gather buffer failed";
+        return SV_ERR_CUDA;
+    }
+    cudaMemcpyAsync(d, local, bytes, cudaMemcpyHostToDevice, s->stream);
+    const ncclResult_t r = ncclAllGather(d, d + bytes, bytes, ncclUint8, (ncclComm_t)s->comm, s->stream);
+    all.assign(bytes * s->world, 0);
+    cudaMemcpyAsync(all.data(), d + bytes, bytes * s->world, cudaMemcpyDeviceToHost, s->stream);
+    const cudaError_t e = cudaStreamSynchronize(s->stream);
+    cudaFree(d);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather", err);
+    if (e != cudaSuccess) {
+        err = std::string("allgather: ") + cudaGetErrorString(e);
+        return SV_ERR_CUDA;
+    }
+    return SV_OK;
+}
+
+sv_status comm_barrier(sv_state_s* s, std::string& err) {
+    const ncclResult_t r = ncclAllReduce(s->xflag, s->xflag, 1, ncclInt32, ncclSum, (ncclComm_t)s->comm, s->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce (barrier)", err);
+    return SV_OK;
+}
+
 }  // namespace svb

@@ -18,6 +18,13 @@ sv_status comm_sendrecv(sv_state_s* s, int peer, const void* send, void* recv, s
 sv_status comm_allgather_doubles(sv_state_s* s, const double* local, size_t count, std::vector<double>& all,
                                  std::string& err);
 
+// every rank's `bytes` host bytes, gathered in rank order (host in/out)
+sv_status comm_allgather_bytes(sv_state_s* s, const void* local, size_t bytes, std::vector<unsigned char>& all,
+                               std::string& err);
+// stream-ordered barrier: a one-word all-reduce on the state's stream (every rank's earlier
+// kernels, including their stores into peer memory, complete before anyone's later ones start)
+sv_status comm_barrier(sv_state_s* s, std::string& err);
+
 }  // namespace svb
 
 sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats);

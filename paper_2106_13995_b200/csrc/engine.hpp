@@ -64,6 +64,7 @@ struct RunOpts {
     bool check_unitary = false;
     bool use_graph = false;
     bool profile = false;
+    int exchange = 0;            // sharded: 0 = fused peer-memory exchange when available, 1 = NCCL
     bool use_jit() const { return fuse && force_kernel == SV_KERNEL_AUTO; }
 };
 
@@ -115,6 +116,8 @@ struct PassPlan {
     std::shared_ptr<TileSym> sym;        // TILE: the symbolic pass
     void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
     void* jit_fn_basis = nullptr;        // TILE, first pass: variant whose input is a basis state
+    int xS = -1;                         // TILE feeding an exchange: local bits below xS stay (f2)
+    void* jit_fn_x = nullptr;            // TILE, xS >= 0: variant storing into the peers' buffers
     int jit_threads = 0;
     size_t jit_smem = 0;
     bool jit_persistent = false;         // TILE: persistent grid (prefetching kernel)

@@ -789,7 +789,7 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 }  // namespace
 
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc, bool basis_in) {
+                            int& tpc, bool basis_in, int xS) {
     Em e;
     e.dbl = sym.dbl;
     const int rb = sym.rb, R = 1 << rb;
@@ -797,7 +797,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     const int tb = m - rb;
     const int tthreads = 1 << tb;  // threads per tile
     const bool multi = sym.stages.size() > 1;
-    const bool pf = !basis_in && prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
+    const bool pf = !basis_in && xS < 0 && prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
                     ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)tthreads == 0;
     persistent = pf;
     const size_t tile_bytes = ((size_t)1 << m) * (sym.dbl ? 16 : 8);
@@ -844,9 +844,13 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     size_t first = 0;
     if (pf)
         while (first + 1 < sym.stages.size() && sym.stages[first].ops.empty()) ++first;  // I/O-only stage
+    // xS >= 0: fused exchange -- the pass stores every amplitude straight to
+    // where the global<->local swap puts it: local index a on rank r (top local bits c = a >> xS)
+    // goes to rank c at (a & (2^xS - 1)) | r << xS, through the peers' second buffers
+    if (xS >= 0) o << "struct XT { C* p[8]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
       << (pf ? std::max(1, min_blocks(threads) / 2) : min_blocks(threads)) << ") svpass(C* __restrict__ psi"
-      << (basis_in ? ",unsigned long long kb" : "") << "){\n";
+      << (basis_in ? ",unsigned long long kb" : "") << (xS >= 0 ? ",const XT xo,unsigned xr" : "") << "){\n";
     if (pf) o << "extern __shared__ C sm[];\n";
     else if (multi && tpc > 1) o << "extern __shared__ C sm_[];\nC* sm=sm_+((threadIdx.x>>" << tb << ")<<" << m << ");\n";
     else if (multi) o << "extern __shared__ C sm[];\n";
@@ -1124,7 +1128,29 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                     goff[s] = go;
                 }
             }
-            for (int s = 0; s < R; ++s) o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
+            if (xS < 0) {
+                for (int s = 0; s < R; ++s) o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
+            } else {
+                // store bits above xS-1 select the destination rank; when no tile qubit lands
+                // there the whole tile goes to one peer (its rank = the tile base's top bits)
+                bool tile_high = false;
+                for (int q : sym.tq) {
+                    const int oq = sym.out_perm.empty() ? q : sym.out_perm[q];
+                    tile_high |= oq >= xS;
+                }
+                const std::string M = std::to_string((1ull << xS) - 1) + "ull";
+                if (!tile_high) {
+                    o << "{const unsigned long long h_=base>>" << xS << ";C* ob_=xo.p[h_]+(((long long)xr-(long long)h_)<<"
+                      << xS << ");\n";
+                    for (int s = 0; s < R; ++s) o << "ob_[g+" << goff[s] << "ull]=" << reg(s) << ";";
+                    o << "}";
+                } else {
+                    for (int s = 0; s < R; ++s)
+                        o << "{const unsigned long long a_=g+" << goff[s] << "ull;xo.p[a_>>" << xS << "][(a_&" << M
+                          << ")|((unsigned long long)xr<<" << xS << ")]=" << reg(s) << ";}";
+                }
+                o << "\n__threadfence_system();";  // peer stores performed before the barrier
+            }
             o << "\n";
         } else {
             // unit phases are tied to this stage's register numbering: apply before re-distribution
@@ -1274,6 +1300,20 @@ std::string gen_perm_source(const PassPlan& pp, bool dbl, int& threads) {
     return o.str();
 }
 
+// fused-exchange variants of the passes that feed a global<->local swap
+static sv_status jit_prepare_x(Schedule& sc, std::string& err) {
+    for (PassPlan& pp : sc.passes) {
+        if (pp.kind != PassPlan::TILE || !pp.sym || pp.xS < 0 || pp.jit_fn_x || pp.jit_persistent) continue;
+        int th, tpc;
+        size_t sm;
+        bool pers;
+        const std::string src = gen_pass_source(*pp.sym, pp.ntiles, th, sm, pers, tpc, false, pp.xS);
+        const sv_status r = jit_compile(src, sm, &pp.jit_fn_x, err);
+        if (r != SV_OK) return r;
+    }
+    return SV_OK;
+}
+
 sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
     std::vector<PassPlan*> todo;
     for (PassPlan& pp : sc.passes)
@@ -1283,7 +1323,7 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
                        !sc.passes[0].jit_fn_basis)
                           ? &sc.passes[0]
                           : nullptr;
-    if (todo.empty() && !first) return SV_OK;
+    if (todo.empty() && !first) return jit_prepare_x(sc, err);
     std::vector<std::string> srcs(todo.size() + (first ? 1 : 0));
     for (size_t i = 0; i < todo.size(); ++i) {
         if (todo[i]->kind == PassPlan::PERM) {
@@ -1339,7 +1379,7 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
             todo[i]->jit_grid = (unsigned)std::min<uint64_t>(grid, todo[i]->ntiles);
         }
     }
-    return SV_OK;
+    return jit_prepare_x(sc, err);
 }
 
 cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream) {
@@ -1353,6 +1393,15 @@ cudaError_t jit_launch_basis(const PassPlan& pp, void* psi, uint64_t kb, cudaStr
     void* args[] = {&psi, &k};
     return cudaLaunchKernel(pp.jit_fn_basis, dim3(pp.jit_grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem,
                             stream);
+}
+
+cudaError_t jit_launch_x(const PassPlan& pp, void* psi, void* const outs[8], unsigned rank, cudaStream_t stream) {
+    struct XT {
+        void* p[8];
+    } xo;
+    for (int i = 0; i < 8; ++i) xo.p[i] = outs[i];
+    void* args[] = {&psi, &xo, &rank};
+    return cudaLaunchKernel(pp.jit_fn_x, dim3(pp.jit_grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem, stream);
 }
 
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {

@@ -405,6 +405,23 @@ __global__ void fill_kernel(typename V2<real>::t* __restrict__ psi, uint64_t N, 
         psi[i] = val;
 }
 
+// ------------------------------------------------------------------ peer-memory exchange (f2)
+// Swap of the g global bits with the g top local bits as one copy over NVLink peer memory:
+// local 16-byte chunk a of rank r (top local bits c = a >> S) is stored to rank c's second
+// buffer at (a & (2^S - 1)) | r << S.  Used when the batch before the exchange ends in a pass
+// that cannot store remotely itself (dense-k or no pass at all).
+struct PeerTable {
+    uint4* p[8];
+};
+
+__global__ void __launch_bounds__(256) exchange_copy_kernel(const uint4* __restrict__ in, PeerTable out, uint64_t N,
+                                                            int S, unsigned rank) {
+    const uint64_t M = (1ull << S) - 1;
+    for (uint64_t a = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; a < N; a += (uint64_t)gridDim.x * blockDim.x)
+        out.p[a >> S][(a & M) | ((uint64_t)rank << S)] = in[a];
+    __threadfence_system();  // peer stores performed before the barrier that follows
+}
+
 // ------------------------------------------------------------------ readout (K8)
 // Block (k, chunk) sums |a|^2 over the rest-indices of one chunk for the subset value k,
 // each thread sequentially over a fixed strided set, then a fixed-order tree in smem.
@@ -616,6 +633,19 @@ cudaError_t launch_fill(bool dbl, void* psi, uint64_t N, double re, double im, c
     else
         fill_kernel<float><<<grid_for(N, threads), threads, 0, st>>>(reinterpret_cast<float2*>(psi), N, (float)re,
                                                                       (float)im);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_exchange_copy(const void* in, void* const outs[8], uint64_t bytes, int nl, int g, int amp_bytes,
+                                 unsigned rank, cudaStream_t st) {
+    // in 16-byte chunks: a chunk never straddles a rank boundary (chunks per rank >= 1)
+    const int cshift = amp_bytes == 16 ? 0 : 1;  // amplitudes per chunk = 2^cshift
+    const int S = nl - g - cshift;
+    if (S < 0) return cudaErrorInvalidValue;
+    PeerTable t;
+    for (int i = 0; i < 8; ++i) t.p[i] = reinterpret_cast<uint4*>(outs[i]);
+    const uint64_t N = bytes / 16;
+    exchange_copy_kernel<<<grid_for(N, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(in), t, N, S, rank);
     return cudaGetLastError();
 }
 

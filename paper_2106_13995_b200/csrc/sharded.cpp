@@ -49,10 +49,126 @@ LOp phys_swap(int a, int b) {
     return op;
 }
 
-// launch one shard's schedule
-sv_status run_sched(sv_state_s* s, int i, const Schedule& sc, sv_run_stats* st, std::string& err) {
+// Fused peer-memory exchange: set up the second buffer of every rank and
+// map the peers' buffer pairs (CUDA IPC over NVLink; virtual: offsets into one allocation).
+// Collective.  Leaves xmode = 1 when every rank succeeded, else 2 (NCCL exchange).
+sv_status peer_setup(sv_state_s* s, std::string& err) {
+    if (s->xmode) return SV_OK;
+    const size_t shard = (size_t)s->local_amps() * s->amp_bytes();
+    const size_t bytes = s->virt ? shard * s->world : shard;
+    bool ok = s->world <= 8 && s->owned;
+    if (ok && !s->d2) {
+        if (cudaMalloc(&s->d2, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            s->d2 = nullptr;
+            ok = false;
+        }
+    }
+    if (s->virt) {
+        s->xmode = ok ? 1 : 2;
+        if (ok)
+            for (int c = 0; c < s->world; ++c) {
+                s->xpeer[0][c] = (char*)s->d + (size_t)c * shard;
+                s->xpeer[1][c] = (char*)s->d2 + (size_t)c * shard;
+            }
+        s->xcur = 0;
+        return SV_OK;
+    }
+    if (ok && !s->xflag) {
+        if (cudaMalloc(&s->xflag, 16) != cudaSuccess || cudaMemset(s->xflag, 0, 16) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+        }
+    }
+    struct Msg {
+        int ok;
+        int pad;
+        cudaIpcMemHandle_t h[2];
+    } m{};
+    m.ok = ok;
+    if (ok && (cudaIpcGetMemHandle(&m.h[0], s->d) != cudaSuccess || cudaIpcGetMemHandle(&m.h[1], s->d2) != cudaSuccess)) {
+        cudaGetLastError();
+        m.ok = 0;
+    }
+    std::vector<unsigned char> all;
+    sv_status r = comm_allgather_bytes(s, &m, sizeof m, all, err);
+    if (r != SV_OK) return r;
+    bool all_ok = true;
+    for (int c = 0; c < s->world; ++c) all_ok &= reinterpret_cast<const Msg*>(all.data())[c].ok != 0;
+    int opened = 1;
+    if (all_ok) {
+        for (int c = 0; c < s->world && opened; ++c) {
+            const Msg& pm = reinterpret_cast<const Msg*>(all.data())[c];
+            for (int b = 0; b < 2; ++b) {
+                if (c == s->rank) {
+                    s->xpeer[b][c] = b == 0 ? s->d : s->d2;
+                    continue;
+                }
+                void* p = nullptr;
+                if (cudaIpcOpenMemHandle(&p, pm.h[b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    opened = 0;
+                    break;
+                }
+                s->ipc_open.push_back(p);
+                s->xpeer[b][c] = p;
+            }
+        }
+        // every rank must have mapped every peer
+        std::vector<unsigned char> flags;
+        r = comm_allgather_bytes(s, &opened, sizeof opened, flags, err);
+        if (r != SV_OK) return r;
+        for (int c = 0; c < s->world; ++c) all_ok &= reinterpret_cast<const int*>(flags.data())[c] != 0;
+    }
+    if (!all_ok) {
+        for (void* q : s->ipc_open) cudaIpcCloseMemHandle(q);
+        s->ipc_open.clear();
+    }
+    s->xmode = all_ok ? 1 : 2;
+    s->xcur = 0;
+    return SV_OK;
+}
+
+// After every rank's exchange-feeding pass: barrier, then the second buffers hold the state.
+sv_status peer_flip(sv_state_s* s, sv_run_stats* st, std::string& err) {
+    if (!s->virt) {
+        const sv_status r = comm_barrier(s, err);
+        if (r != SV_OK) return r;
+    }
+    std::swap(s->d, s->d2);
+    s->xcur ^= 1;
+    if (st) {
+        st->swaps++;
+        st->nvlink_bytes += (uint64_t)((s->local_amps() >> s->g) * s->amp_bytes()) * (s->world - 1);
+    }
+    return SV_OK;
+}
+
+// launch one shard's schedule; outs != null: the schedule feeds a fused exchange -- its last
+// pass stores into the peers' second buffers (or, if it cannot, a peer copy follows)
+sv_status run_sched(sv_state_s* s, int i, const Schedule& sc, sv_run_stats* st, std::string& err,
+                    void* const* outs = nullptr) {
     void* psi = s->shard_ptr(i);
-    for (const PassPlan& pp : sc.passes) {
+    const unsigned rank = (unsigned)rank_of(s, i);
+    bool stored = false;
+    for (size_t pi = 0; pi < sc.passes.size(); ++pi) {
+        const PassPlan& pp = sc.passes[pi];
+        const bool last = pi + 1 == sc.passes.size();
+        if (outs && last && pp.jit_fn_x) {
+            const cudaError_t e = jit_launch_x(pp, psi, outs, rank, s->stream);
+            if (e != cudaSuccess) {
+                err = std::string("fused exchange pass launch: ") + cudaGetErrorString(e);
+                return SV_ERR_CUDA;
+            }
+            stored = true;
+            if (st && i == 0) {
+                st->passes++;
+                st->launches++;
+                st->stages += pp.nstages;
+                st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+            }
+            continue;
+        }
         cudaError_t e = (pp.kind == PassPlan::TILE && pp.jit_fn) ? jit_launch(pp, psi, s->stream)
                         : pp.kind == PassPlan::TILE
                             ? launch_tile_pass(s->dbl, pp.rb, psi, pp.params.data(), pp.m, pp.nstages, pp.ntiles,
@@ -67,6 +183,19 @@ sv_status run_sched(sv_state_s* s, int i, const Schedule& sc, sv_run_stats* st, 
             st->launches++;
             st->stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
             st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+        }
+    }
+    if (outs && !stored) {
+        const size_t shard = (size_t)s->local_amps() * s->amp_bytes();
+        const cudaError_t e =
+            launch_exchange_copy(psi, outs, shard, s->nl, s->g, (int)s->amp_bytes(), rank, s->stream);
+        if (e != cudaSuccess) {
+            err = std::string("exchange copy launch: ") + cudaGetErrorString(e);
+            return SV_ERR_CUDA;
+        }
+        if (st && i == 0) {
+            st->launches++;
+            st->hbm_bytes += 2ull * shard;
         }
     }
     return SV_OK;
@@ -210,17 +339,24 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
         p->shard_cache.push_back(std::move(plan));
         sp = &p->shard_cache.back();
     }
-    for (ShardStep& step : sp->steps) {
+    if (o.exchange == 0 && sp->swaps > 0 && !s->xmode) {
+        const sv_status r = peer_setup(s, err);
+        if (r != SV_OK) return set_err(r, err);
+    }
+    const bool peer = o.exchange == 0 && s->xmode == 1;
+    for (size_t si = 0; si < sp->steps.size(); ++si) {
+        ShardStep& step = sp->steps[si];
         sv_status r;
         if (step.exchange) {
-            r = exchange_all(s, stats, err);
+            r = peer ? peer_flip(s, stats, err) : exchange_all(s, stats, err);
         } else {
+            const bool feeds = peer && si + 1 < sp->steps.size() && sp->steps[si + 1].exchange;
             for (size_t i = 0; i < step.sched.size(); ++i) {
                 if (o.use_jit()) {
                     r = jit_prepare(step.sched[i], err);
                     if (r != SV_OK) return set_err(r, err);
                 }
-                r = run_sched(s, (int)i, step.sched[i], stats, err);
+                r = run_sched(s, (int)i, step.sched[i], stats, err, feeds ? s->xpeer[s->xcur ^ 1] : nullptr);
                 if (r != SV_OK) return set_err(r, err);
             }
             r = SV_OK;
@@ -319,6 +455,10 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
             Schedule sc;
             const sv_status r = build_schedule(ops[i], ctx_for(ranks[i]), o, sc, err);
             if (r != SV_OK) return r;
+            // the batch's last pass feeds the exchange: give it the remote-store variant
+            if (!deferred.empty() && o.exchange == 0 && !sc.passes.empty() &&
+                sc.passes.back().kind == PassPlan::TILE && sc.passes.back().sym)
+                sc.passes.back().xS = nl - g;
             batch.sched.push_back(std::move(sc));
         }
         out.steps.push_back(std::move(batch));

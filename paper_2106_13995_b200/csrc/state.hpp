@@ -27,6 +27,14 @@ struct sv_state_s {
     void* comm = nullptr;   // ncclComm_t (real sharding)
     void* xbuf = nullptr;   // exchange staging buffer (real sharding)
     size_t xbuf_bytes = 0;
+    // fused peer-memory exchange: d and d2 are this rank's buffer pair
+    // (d2 of the full virtual size when virtual); xpeer[b][c] = rank c's buffer b (CUDA IPC
+    // for real ranks), xcur = which of the pair d is -- identical on every rank
+    int xmode = 0;          // 0 = not set up, 1 = peer memory, 2 = NCCL send/recv (fallback / opted)
+    int xcur = 0;
+    void* xpeer[2][8] = {};
+    std::vector<void*> ipc_open;  // peer mappings to close
+    void* xflag = nullptr;        // 4-byte device word for the stream-ordered barrier
     std::vector<int> phys;  // logical qubit -> physical bit
     double* d_scratch = nullptr;
     size_t scratch_doubles = 0;

@@ -40,6 +40,9 @@ uint64_t marginal_partials(const MarginalParams& P);  // partial-sum doubles lau
 cudaError_t launch_tile_pass(bool dbl, int rb, void* psi, const void* params, int m, int nstages, uint64_t ntiles,
                              cudaStream_t st);
 cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t groups, cudaStream_t st);
+// f2: store the local shard to the peers' second buffers at the swapped positions
+cudaError_t launch_exchange_copy(const void* in, void* const outs[8], uint64_t bytes, int nl, int g, int amp_bytes,
+                                 unsigned rank, cudaStream_t st);
 cudaError_t launch_fill(bool dbl, void* psi, uint64_t N, double re, double im, cudaStream_t st);
 cudaError_t launch_marginal(bool dbl, const void* psi, const MarginalParams& P, double* partial, double* out,
                             cudaStream_t st);

@@ -30,9 +30,9 @@ def _dtype(d) -> int:
 
 
 def make_opts(fuse: bool = True, tile_qubits: int = 0, force_kernel: int = 0, check_unitary: bool = False,
-              use_graph: bool = False, profile: bool = False) -> RunOpts:
+              use_graph: bool = False, profile: bool = False, exchange: int = 0) -> RunOpts:
     return RunOpts(int(fuse), int(tile_qubits), 0, int(force_kernel), int(check_unitary), int(use_graph),
-                   int(profile))
+                   int(profile), int(exchange))
 
 
 def _stream_ptr(stream) -> Optional[int]:

@@ -93,3 +93,70 @@ def test_sharded_apply_gate_on_global_qubit(P):
     ref = oracle.apply_gate(psi0.copy(), U, [9, 2], [8])
     ref = oracle.apply_gate(ref, np.diag([1, 1j]), [9])
     assert np.max(np.abs(got - ref)) <= 1e-13
+
+
+# ---------------------------------------------------------------- fused exchange
+# The default exchange stores the last pass before a swap straight into the peers' second
+# buffers (the remote-store pass variant, or a peer copy after a non-generated pass); the
+# ablation (exchange=1) runs the same passes in place and then swaps chunks.  The arithmetic
+# is the same, so the two must agree bit for bit, and both must match the oracle.
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_fused_exchange_bit_identical_to_copy_exchange(P, world, dtype):
+    n = 20
+    c = W.supremacy(5, 4, 14, seed=11 + world)
+    text = W.to_text(c)
+    got_f, st_f, _ = run_virtual(P, text, n, world, dtype)
+    got_c, st_c, _ = run_virtual(P, text, n, world, dtype, exchange=1)
+    assert st_f["swaps"] >= 1 and st_f["swaps"] == st_c["swaps"]
+    assert np.array_equal(got_f.view(np.uint8), got_c.view(np.uint8))
+    ref = oracle.simulate(text)
+    assert_close(got_f, ref, dtype, W.gate_count(c))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_fused_exchange_after_interpreter_passes(P, world):
+    # fuse=False: per-gate interpreter passes (no generated kernel) -> the peer copy kernel
+    n = 12
+    c = W.random_circuit(n, 80, 77 + world, max_k=3, max_controls=2)
+    text = W.to_text(c)
+    psi0 = W.random_state(n, 5)
+    ref = oracle.simulate(text, psi0)
+    got_f, st_f, _ = run_virtual(P, text, n, world, "c128", psi0, fuse=False)
+    got_c, _, _ = run_virtual(P, text, n, world, "c128", psi0, fuse=False, exchange=1)
+    assert st_f["swaps"] >= 1
+    assert np.array_equal(got_f, got_c)
+    assert_close(got_f, ref, "c128", W.gate_count(c))
+
+
+def test_fused_exchange_multiplier_bit_exact(P):
+    c = W.multiplier(3)
+    text = W.to_text(c)
+    for a, b in [(3, 5), (7, 6)]:
+        psi0 = np.zeros(1 << c.n, complex)
+        psi0[a | (b << 3)] = 1
+        ref = oracle.simulate(text, psi0)
+        for world in (2, 8):
+            got, st, _ = run_virtual(P, text, c.n, world, "c128", psi0)
+            assert np.array_equal(got, ref), (a, b, world)
+
+
+def test_fused_exchange_repeated_runs_and_readout(P):
+    # several circuits on one state: the buffer pair flips at every swap and stays consistent
+    n, world = 16, 4
+    c = W.supremacy(4, 4, 8, seed=21)
+    text = W.to_text(c)
+    psi0 = W.random_state(n, 9)
+    ref = psi0.copy()
+    for _ in range(3):
+        ref = oracle.simulate(text, ref)
+    with P.StateVector.virtual_sharded(n, world, "c128") as sv:
+        sv.set_amplitudes(psi0)
+        swaps = 0
+        for _ in range(3):
+            swaps += sv.apply_circuit(text)["swaps"]
+        got = sv.amplitudes()
+        assert abs(sv.norm() - 1) <= 1e-12
+    assert swaps >= 3
+    assert np.max(np.abs(got - ref)) <= 1e-12
