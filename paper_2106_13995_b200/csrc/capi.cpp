@@ -201,12 +201,12 @@ sv_status plan_schedule(sv_plan_s* p) {
     Schedule perm;
     const bool have_perm = !p->opts.use_graph && build_perm_schedule(p->circ, ctx, p->opts, perm);
     std::vector<LOp> ops;
-    for (size_t i = 0; i < p->circ.gates.size(); ++i) {
+    for (size_t i = 0; i < p->lcirc.gates.size(); ++i) {
         bool needs_global = false;
-        const sv_status st = lower_gate(p->circ.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
+        const sv_status st = lower_gate(p->lcirc.gates[i], (int)i, ctx, p->opts, ops, needs_global, err);
         if (st != SV_OK) return fail(st, err);
     }
-    const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err, &p->circ);
+    const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err, &p->lcirc);
     if (st != SV_OK) return fail(st, err);
     // a reversible circuit: one gather pass, unless its scattered reads cost more than the
     // fused tile passes (both estimated in HBM passes)
@@ -462,6 +462,7 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
     sv_plan_s plan;
     plan.circ.n = s->n;
     plan.circ.gates.push_back(std::move(g));
+    plan.lcirc = plan.circ;
     plan.dtype = s->dtype;
     plan.opts.fuse = false;
     return sv_plan_apply(s, &plan, nullptr);
@@ -482,6 +483,7 @@ sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts
     }
     p->dtype = dtype;
     p->opts = to_opts(opts);
+    p->lcirc = merge_single_qubit(p->circ);
     const sv_status s2 = plan_schedule(p);
     if (s2 != SV_OK) {
         delete p;
@@ -544,7 +546,7 @@ sv_status sv_plan_shard_info(sv_plan p, int world, uint64_t* swaps, uint64_t* ba
     if (o.force_kernel == SV_KERNEL_DENSE) o.force_kernel = SV_KERNEL_PER_GATE;
     ShardPlan sp;
     std::string err;
-    const sv_status st = shard_plan(p->circ, o, n, nl, world, p->dtype == SV_C128, {0}, phys, sp, err);
+    const sv_status st = shard_plan(p->lcirc, o, n, nl, world, p->dtype == SV_C128, {0}, phys, sp, err);
     if (st != SV_OK) return fail(st, err);
     uint64_t nb = 0, np = 0;
     for (const ShardStep& s : sp.steps)

@@ -34,6 +34,12 @@ sv_status parse_ir(const char* text, Circuit& out, std::string& err);
 // Named gate table; false if unknown.
 bool named_gate(const std::string& name, int& ncontrols, int& k, std::vector<cd>& U);
 
+// U = f V with every entry of V in {0, +-1, +-i} (within 1e-12 |f|); f = the first nonzero
+// entry.  The "unit class": Paulis, H, SqrtX/SqrtY, S, Z and their products.
+bool unit_factor(const std::vector<cd>& U, std::vector<cd>& V, cd& f);
+// Runs of uncontrolled unit-class 1-qubit gates on a qubit merged into one gate (planner.cpp).
+Circuit merge_single_qubit(const Circuit& c);
+
 // ------------------------------------------------------------------ lowered ops
 enum LKind { L_REG = 0, L_DENSEK = 1 };
 

@@ -563,6 +563,14 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
             cd f = 1;
             if (op.kind == OP_U1 || op.kind == OP_U2 || op.kind == OP_U3 || op.kind == OP_U4) {
                 M = op.coef;
+                // a unit-class matrix (U = f V, V in {0, +-1, +-i}; e.g. merged Clifford runs):
+                // unscaled butterfly with f deferred, like the named gates
+                std::vector<cd> V;
+                cd uf;
+                if (!controlled && unit_factor(op.coef, V, uf)) {
+                    M = V;
+                    f = uf;
+                }
             } else if (op.kind == OP_SWAP) {
                 M = {1, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 0, 1};
             } else {

@@ -334,7 +334,7 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
         if (c.world == s->world && c.dbl == s->dbl && c.ranks == ranks && c.start_phys == s->phys) sp = &c;
     if (!sp) {
         ShardPlan plan;
-        const sv_status r = shard_plan(p->circ, o, s->n, s->nl, s->world, s->dbl, ranks, s->phys, plan, err);
+        const sv_status r = shard_plan(p->lcirc, o, s->n, s->nl, s->world, s->dbl, ranks, s->phys, plan, err);
         if (r != SV_OK) return set_err(r, err);
         p->shard_cache.push_back(std::move(plan));
         sp = &p->shard_cache.back();

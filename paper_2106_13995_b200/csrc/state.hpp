@@ -71,7 +71,8 @@ sv_status shard_plan(const svb::Circuit& circ, const svb::RunOpts& o, int n, int
 
 struct sv_plan_s {
     std::list<ShardPlan> shard_cache;   // sharded schedules by (world, ranks, map at entry)
-    svb::Circuit circ;
+    svb::Circuit circ;                  // as parsed (gate counts, permutation pass)
+    svb::Circuit lcirc;                 // what is lowered: 1-qubit unit-class runs merged
     sv_dtype dtype = SV_C64;
     svb::RunOpts opts;
     // schedule cache for the identity qubit map on one unsharded GPU

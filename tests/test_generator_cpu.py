@@ -102,3 +102,39 @@ def test_to_logical_roundtrip():
     y = np.zeros_like(x)
     y[phys] = x
     assert np.array_equal(to_logical(y, qmap, n), x)
+
+
+def clifford_run_circuit(n, ngates, seed):
+    """Long same-qubit runs of unit-class 1-qubit gates (Paulis, H, S, SqrtX/SqrtY and inverses,
+    and unit-class custom U with a global phase), mixed with T and CZ -- the runs the planner
+    merges into one butterfly or one permutation/phase (planner.cpp merge_single_qubit)."""
+    rng = np.random.default_rng(seed)
+    one = ["X", "Y", "Z", "H", "S", "Sdg", "SqrtX", "SqrtY", "SqrtXdg", "SqrtYdg"]
+    gates = []
+    for _ in range(ngates):
+        u = rng.random()
+        if u < 0.08:
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            gates.append(W.GateSpec("CZ", (a, b)))
+        elif u < 0.14:
+            gates.append(W.GateSpec("T", (int(rng.integers(n)),)))
+        elif u < 0.24:
+            ph = np.exp(1j * rng.uniform(0, 2 * np.pi))
+            m = ph * np.array([[1, 1j], [1j, 1]]) / np.sqrt(2) if rng.random() < 0.5 else ph * np.array([[0, 1j], [1, 0]])
+            gates.append(W.GateSpec("U", (int(rng.integers(n)),), (), tuple(complex(x) for x in m.reshape(-1))))
+        else:
+            # bias towards a few qubits so that long runs form
+            q = int(rng.integers(min(n, 3))) if rng.random() < 0.6 else int(rng.integers(n))
+            gates.append(W.GateSpec(one[rng.integers(len(one))], (q,)))
+    return W.Circuit(n, [[g] for g in gates], "custom", {"seed": seed})
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n,seed", [(5, 0), (13, 1)])
+def test_merged_single_qubit_runs(P, dtype, n, seed):
+    c = clifford_run_circuit(n, 300, seed)
+    text = W.to_text(c)
+    psi = W.random_state(n, seed + 20)
+    psi = W.round_to_c64(psi) if dtype == "c64" else psi
+    got, _ = _emulated(P, text, n, dtype, psi)
+    assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))

@@ -173,6 +173,21 @@ def test_phase_polynomial_circuits(P, dtype, n, seed):
         assert_close(got, ref, dtype, W.gate_count(c))
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n,seed", [(4, 0), (15, 1), (21, 2)])
+def test_merged_single_qubit_runs(P, dtype, n, seed):
+    # runs of unit-class 1-qubit gates merged by the planner (merge_single_qubit), incl. custom
+    # U with a global phase; fused and per-gate (unmerged lowering of single gates) both
+    from tests.test_generator_cpu import clifford_run_circuit
+    c = clifford_run_circuit(n, 400, seed)
+    text = W.to_text(c)
+    psi0 = input_for(n, seed + 30, dtype)
+    ref = oracle.simulate(text, psi0)
+    for mode in ({}, {"fuse": False}):
+        got, _ = run_gpu(P, text, n, dtype, psi0=psi0, **mode)
+        assert_close(got, ref, dtype, W.gate_count(c))
+
+
 def test_qft_20q_vs_oracle(P):
     c = W.qft(20)
     text = W.to_text(c)
