@@ -669,11 +669,14 @@ double op_cost(const LOp& op) {
 double heavy_pass_cost(bool dbl) {
     static double b = [] {
         const char* e = getenv("SV_HEAVY_COST");
-        return e ? atof(e) : 200.0;
+        // measured (profiles/r01_heavy_sweep.txt, after the 1-qubit merge): 30 q supremacy
+        // c64 25.9 ms at 200, 24.5 at 160, 24.8 at 130, 25.8 at 100
+        return e ? atof(e) : 160.0;
     }();
     static double b2 = [] {
         const char* e = getenv("SV_HEAVY_COST128");
-        return e ? atof(e) : 200.0;
+        // c128: 52.7 ms at 200, 52.6 at 160, 54.6 at 130, 57.4 at 100
+        return e ? atof(e) : 160.0;
     }();
     return dbl ? b2 : b;
 }
