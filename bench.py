@@ -142,12 +142,39 @@ ALG_OPS = {"H": 2, "SqrtX": 2, "SqrtY": 2, "SqrtXdg": 2, "SqrtYdg": 2, "T": 1, "
            "S": 0, "Sdg": 0, "X": 0, "CNOT": 0, "CX": 0, "SWAP": 0, "CCX": 0, "Toffoli": 0, "CCNOT": 0}
 
 
+# Unscaled matrices of the unit-class named gates (entries in {0, +-1, +-i} up to a factor).
+# A run of them on one qubit is merged by the planner into one gate (planner.cpp
+# merge_single_qubit): one butterfly (2) if the product has four nonzero entries, else a
+# permutation/phase (0).  The algorithmic count follows the merged circuit.
+_UNIT_1Q = {"H": ((1, 1), (1, -1)), "SqrtX": ((1, -1j), (-1j, 1)), "SqrtXdg": ((1, 1j), (1j, 1)),
+            "SqrtY": ((1, -1), (1, 1)), "SqrtYdg": ((1, 1), (-1, 1)), "X": ((0, 1), (1, 0)),
+            "Y": ((0, -1j), (1j, 0)), "Z": ((1, 0), (0, -1)), "S": ((1, 0), (0, 1j)), "Sdg": ((1, 0), (0, -1j))}
+
+
 def alg_ops_per_amp(circuit, passes: int):
+    import numpy as np
     ops = 0.0
+    run = {}  # qubit -> product of the pending unit-class run
+
+    def flush(q):
+        nonlocal ops
+        m = run.pop(q, None)
+        if m is not None:
+            ops += 2.0 if np.all(np.abs(m) > 1e-9) else 0.0
+
     for g in circuit.gates:
         if g.name not in ALG_OPS or g.matrix is not None or (g.controls and ALG_OPS[g.name]):
             return None
+        qs = tuple(g.controls) + tuple(g.qubits)
+        if g.name in _UNIT_1Q and len(qs) == 1:
+            m = np.array(_UNIT_1Q[g.name], dtype=complex)
+            run[qs[0]] = m @ run[qs[0]] if qs[0] in run else m
+            continue
+        for q in qs:
+            flush(q)
         ops += ALG_OPS[g.name]
+    for q in list(run):
+        flush(q)
     return ops + (2.0 * passes if ops > 0 else 0.0)
 
 

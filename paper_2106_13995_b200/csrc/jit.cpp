@@ -764,13 +764,16 @@ int tiles_per_cta() {
     return v;
 }
 
-// CTAs per SM the register allocation must allow (SV_MIN_WARPS: resident warps per SM)
-int min_blocks(int threads) {
+// CTAs per SM the register allocation must allow (SV_MIN_WARPS: resident warps per SM).
+// Measured (profiles/r01_min_warps.txt, 30 q supremacy): c64 24.85 ms at 16 warps, 24.2 at
+// 20, 27.6 at 24; c128 no better than noise at 20, 62 ms at 24 -- 20 (c64) / 16 (c128).
+int min_blocks(int threads, bool dbl) {
     static const int w = [] {
         const char* e = getenv("SV_MIN_WARPS");
-        return e ? atoi(e) : 16;
+        return e ? atoi(e) : 0;
     }();
-    return std::max(1, std::min(32, w * 32 / threads));
+    const int warps = w > 0 ? w : dbl ? 16 : 20;
+    return std::max(1, std::min(32, warps * 32 / threads));
 }
 
 // run-length emission of  sum_i ((t >> i) & 1) << dst[i]
@@ -857,7 +860,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     // goes to rank c at (a & (2^xS - 1)) | r << xS, through the peers' second buffers
     if (xS >= 0) o << "struct XT { C* p[8]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
-      << (pf ? std::max(1, min_blocks(threads) / 2) : min_blocks(threads)) << ") svpass(C* __restrict__ psi"
+      << (pf ? std::max(1, min_blocks(threads, sym.dbl) / 2) : min_blocks(threads, sym.dbl)) << ") svpass(C* __restrict__ psi"
       << (basis_in ? ",unsigned long long kb" : "") << (xS >= 0 ? ",const XT xo,unsigned xr" : "") << "){\n";
     if (pf) o << "extern __shared__ C sm[];\n";
     else if (multi && tpc > 1) o << "extern __shared__ C sm_[];\nC* sm=sm_+((threadIdx.x>>" << tb << ")<<" << m << ");\n";

@@ -29,6 +29,11 @@ __global__ void k(u64* out, u64 seed, float fs) {
             if (MODE == 9) v[i] = F(v[i], 0x3f3504f33f3504f3ull, v[i]);
             if (MODE == 6) dd[i] = dd[i] + dd[(i + 1) % NCH];
             if (MODE == 7) dd[i] = dd[i] * ds + dd[(i + 1) % NCH];
+            // mixes: is the scalar FP32 path (fmalite) free while FADD2 occupies fmaheavy?
+            if (MODE == 10) { v[i] = A(v[i], kk); f[i] = f[i] + fs; }
+            if (MODE == 11) { v[i] = A(v[i], kk); if (i & 1) f[i] = f[i] + fs; }
+            if (MODE == 12) { v[i] = A(v[i], kk); f[i] = f[i] + fs; f[(i + 4) % NCH] = f[(i + 4) % NCH] + fs; }
+            if (MODE == 13) { v[i] = A(v[i], kk); v[i] = A(v[i], kk); f[i] = f[i] + fs; }
         }
     }
     u64 s = 0;
@@ -71,5 +76,10 @@ int main() {
     run<9>("FFMA2 (imm, same reg)", d);
     run<6>("DADD (reg)", d);
     run<7>("DFMA (reg)", d);
+    // mixes: warp-instr counted as NCH per iteration (divide by the mix to get each kind)
+    run<10>("FADD2+FADD 1:1", d);
+    run<11>("FADD2+FADD 2:1", d);
+    run<12>("FADD2+FADD 1:2", d);
+    run<13>("FADD2+FADD 2:1 b", d);
     return 0;
 }
