@@ -95,3 +95,40 @@ def test_31q_multiplier_basis_exact(P):
             assert sv.norm() == 1.0
     a, b = 255, 127
     assert int(ys[-1]) == a | (b << 8) | ((a * b) << 15)
+
+
+def _available_ram():
+    try:
+        return int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    except Exception:
+        return 0
+
+
+def test_30q_bench_circuit_every_amplitude_vs_oracle(P):
+    """The exact bench.py workload (config 3: 30 q supremacy d20, seed 0), launched the way
+    bench.py times it (compiled plan, init_zero deferred into the first pass, fused generated
+    passes), compared with the fp64 oracle amplitude by amplitude over all 2^30 indices, for
+    both dtypes (streamed in chunks; bounds of reading R9)."""
+    need = (16 << 30) + (2 << 30)
+    if _available_ram() < need:
+        pytest.skip(f"host RAM: the 30 q fp64 oracle state needs {need >> 30} GiB")
+    c = W.supremacy(6, 5, 20, seed=0)
+    text = W.to_text(c)
+    G = W.gate_count(c)
+    ref = oracle.simulate(text)  # 16 GiB complex128, all host cores
+    chunk = 1 << 25
+    for dtype in ("c64", "c128"):
+        u = U_C64 if dtype == "c64" else U_C128
+        plan = P.Plan(text, dtype)
+        with P.StateVector(30, dtype) as sv:
+            sv.init_zero()
+            st = sv.apply_plan(plan)
+            mx, l2 = 0.0, 0.0
+            for first in range(0, 1 << 30, chunk):
+                got = sv.amplitudes(first, chunk).astype(np.complex128)
+                d = np.abs(got - ref[first:first + chunk])
+                mx = max(mx, float(d.max()))
+                l2 += float(np.sum(d * d))
+        assert st["passes"] >= 2
+        assert mx <= (1e-4 if dtype == "c64" else 1e-10), (dtype, mx)
+        assert np.sqrt(l2) <= 8 * G * u, (dtype, np.sqrt(l2), 8 * G * u)
