@@ -160,3 +160,49 @@ def test_fused_exchange_repeated_runs_and_readout(P):
         assert abs(sv.norm() - 1) <= 1e-12
     assert swaps >= 3
     assert np.max(np.abs(got - ref)) <= 1e-12
+
+
+# ---------------------------------------------------------------- the bench's weak-scaling workloads
+# bench.py --gpus N runs a (30 + log2 N)-qubit supremacy circuit (7x5 grid, first n sites, 20
+# cycles) with 2^30 amplitudes per GPU.  Here the same sharded plan runs on one GPU through
+# virtual shards of the same size (fused exchange: a second buffer per shard), and the mirror
+# circuit C C^dagger must return |0...0> -- correctness at full per-GPU size.
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_weak_scaling_workload_virtual_mirror(P, world):
+    g = world.bit_length() - 1
+    n = 30 + g
+    c = W.supremacy((n + 4) // 5, 5, 20, seed=0, n=n)
+    G = 2 * W.gate_count(c)
+    u = 2.0 ** -24
+    with P.StateVector.virtual_sharded(n, world, "c64") as sv:
+        st = sv.apply_plan(P.Plan(W.to_text(c), "c64"))
+        assert st["swaps"] >= 1
+        sv.apply_plan(P.Plan(W.to_text(W.inverse(c)), "c64"))
+        a0 = complex(sv.amplitudes(0, 1)[0])
+        head = sv.amplitudes(1, 1 << 16)
+        nrm = sv.norm()
+    assert abs(a0 - 1) <= 8 * G * u
+    assert np.max(np.abs(head)) <= 8 * G * u
+    assert abs(nrm - 1) <= 8 * G * u
+
+
+def test_30q_virtual_sharded_fused_vs_copy_exchange(P):
+    # the 30 q bench circuit over 4 virtual shards: fused and copy exchange bit-identical at
+    # every amplitude (streamed), norm preserved
+    c = W.supremacy(6, 5, 20, seed=0)
+    text = W.to_text(c)
+    outs = []
+    for ex in (0, 1):
+        sv = P.StateVector.virtual_sharded(30, 4, "c64")
+        st = sv.apply_plan(P.Plan(text, "c64", exchange=ex))
+        assert st["swaps"] >= 1
+        outs.append(sv)
+    chunk = 1 << 26
+    for first in range(0, 1 << 30, chunk):
+        a = outs[0].amplitudes(first, chunk)
+        b = outs[1].amplitudes(first, chunk)
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), first
+    assert abs(outs[0].norm() - 1) <= 8 * W.gate_count(c) * 2.0 ** -24
+    for sv in outs:
+        sv.close()
