@@ -206,3 +206,33 @@ def test_30q_virtual_sharded_fused_vs_copy_exchange(P):
     assert abs(outs[0].norm() - 1) <= 8 * W.gate_count(c) * 2.0 ** -24
     for sv in outs:
         sv.close()
+
+
+def test_33q_p8_virtual_matches_single_gpu(P):
+    # P-invariance at the N = 8 weak-scaling size: the 33 q supremacy d20 circuit on one GPU
+    # (64 GiB c64) and over 8 virtual shards agree within the R9 bounds of both runs
+    n, world = 33, 8
+    need = (2 ** n) * 8 + (8 << 30)
+    try:
+        avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    except Exception:
+        avail = 0
+    if avail < need:
+        pytest.skip(f"host RAM: needs {need >> 30} GiB for the single-GPU reference copy")
+    c = W.supremacy(7, 5, 20, seed=0, n=n)
+    text = W.to_text(c)
+    G = W.gate_count(c)
+    with P.StateVector(n, "c64") as sv:
+        sv.apply_circuit(text)
+        ref = sv.amplitudes()
+    chunk = 1 << 28
+    mx, l2 = 0.0, 0.0
+    with P.StateVector.virtual_sharded(n, world, "c64") as sv:
+        st = sv.apply_circuit(text)
+        assert st["swaps"] >= 1
+        for first in range(0, 1 << n, chunk):
+            d = np.abs(sv.amplitudes(first, chunk).astype(np.complex128) - ref[first:first + chunk])
+            mx = max(mx, float(d.max()))
+            l2 += float(np.sum(d * d))
+    assert mx <= 1e-4
+    assert np.sqrt(l2) <= 16 * G * 2.0 ** -24, np.sqrt(l2)
