@@ -71,6 +71,7 @@ struct RunOpts {
     bool use_graph = false;
     bool profile = false;
     int exchange = 0;            // sharded: 0 = fused peer-memory exchange when available, 1 = NCCL
+    bool no_rollout = false;     // internal: planning a rollout (no nested rollouts)
     bool use_jit() const { return fuse && force_kernel == SV_KERNEL_AUTO; }
 };
 

@@ -689,6 +689,16 @@ bool diag_into_regs() {
     return b;
 }
 
+int rollout_k() {
+    static int k = [] {
+        const char* e = getenv("SV_ROLLOUT");
+        // measured (profiles/r01_rollout.txt): 30 q supremacy c128 8 -> 7 passes, 51.7 ->
+        // 46.1-48.6 ms at K = 32 (K = 4 finds nothing); c64 unchanged; planning 1-2 s
+        return e ? atoi(e) : 32;
+    }();
+    return k;
+}
+
 double pass_budget() {
     static double b = [] {
         const char* e = getenv("SV_PASS_BUDGET");
@@ -968,6 +978,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                 if (dn.empty()) sc += 1e6;  // the next pass finishes the circuit
                 return sc + 1e-6 * popc(low & lowmask);
             };
+            std::vector<std::pair<double, uint64_t>> cands;  // (1-step score, low set)
             if (nt <= 20) {
                 uint32_t c = (1u << L) - 1;
                 while (c < (1u << nt)) {
@@ -975,28 +986,73 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                     for (int j = 0; j < nt; ++j)
                         if ((c >> j) & 1) low |= 1ull << tqs[j];
                     const double sc = score_of(low);
+                    cands.push_back({sc, low});
                     if (sc > best) { best = sc; bestmask = low; }
                     const uint32_t u = c & (0u - c), w = c + u;
                     c = w | (((w ^ c) >> 2) / u);
                 }
             }
-            for (int q = 0; q < 64; ++q)
-                if ((bestmask >> q) & 1) lowset.push_back(q);
-            perm.resize(64);
-            for (int q = 0; q < 64; ++q) perm[q] = q;
-            std::vector<int> free_slots;
-            for (int slot = 0; slot < L; ++slot)
-                if (std::find(lowset.begin(), lowset.end(), slot) == lowset.end()) free_slots.push_back(slot);
-            size_t fi = 0;
-            bool moved = false;
-            for (int q : lowset) {
-                if (q < L) continue;
-                const int slot = free_slots[fi++];
-                perm[q] = slot;
-                perm[slot] = q;
-                moved = true;
+            // physical position -> position after this pass for a given bottom set
+            auto perm_for = [&](uint64_t mask, std::vector<int>& ls) {
+                std::vector<int> pm(64);
+                ls.clear();
+                for (int q = 0; q < 64; ++q)
+                    if ((mask >> q) & 1) ls.push_back(q);
+                for (int q = 0; q < 64; ++q) pm[q] = q;
+                std::vector<int> free_slots;
+                for (int slot = 0; slot < L; ++slot)
+                    if (std::find(ls.begin(), ls.end(), slot) == ls.end()) free_slots.push_back(slot);
+                size_t fi = 0;
+                bool moved = false;
+                for (int q : ls) {
+                    if (q < L) continue;
+                    const int slot = free_slots[fi++];
+                    pm[q] = slot;
+                    pm[slot] = q;
+                    moved = true;
+                }
+                if (!moved) pm.clear();
+                return pm;
+            };
+            // Rollout (SV_ROLLOUT = K candidates, 0 = off): the greedy 1-step score can pick a
+            // bottom set that leaves a small tail for an extra pass; plan the rest of the
+            // circuit greedily for each of the K best sets and keep the one with the fewest
+            // passes (ties: the better 1-step score).
+            const int K = rollout_k();
+            if (K > 1 && !o.no_rollout && cands.size() > 1 && best < 1e6) {
+                std::stable_sort(cands.begin(), cands.end(),
+                                 [](const std::pair<double, uint64_t>& a, const std::pair<double, uint64_t>& b) {
+                                     return a.first > b.first;
+                                 });
+                Circuit sub;
+                sub.n = circ->n;
+                {
+                    std::vector<int> g2;
+                    for (int idx : next) g2.push_back(ops[idx].gate);
+                    std::sort(g2.begin(), g2.end());
+                    g2.erase(std::unique(g2.begin(), g2.end()), g2.end());
+                    for (int gi : g2) sub.gates.push_back(circ->gates[gi]);
+                }
+                RunOpts o2 = o;
+                o2.no_rollout = true;
+                size_t best_passes = SIZE_MAX;
+                for (int k = 0; k < K && k < (int)cands.size(); ++k) {
+                    std::vector<int> ls;
+                    const std::vector<int> pm = perm_for(cands[k].second, ls);
+                    Context c2 = ctx;
+                    if (!pm.empty())
+                        for (int& p : c2.phys) p = pm[p];
+                    Schedule s2;
+                    std::vector<LOp> ops2;
+                    std::string e2;
+                    if (build_schedule(ops2, c2, o2, s2, e2, &sub) != SV_OK) continue;
+                    if (s2.passes.size() < best_passes) {
+                        best_passes = s2.passes.size();
+                        bestmask = cands[k].second;
+                    }
+                }
             }
-            if (!moved) perm.clear();
+            perm = perm_for(bestmask, lowset);
         }
         if (getenv("SV_PLAN_DEBUG")) {
             fprintf(stderr, "pass %zu: ops %zu deferred %zu S=", out.passes.size(), pass_ops.size(), next.size());
