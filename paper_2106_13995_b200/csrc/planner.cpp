@@ -732,8 +732,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
         const char* e = getenv("SV_RELABEL");
         return e ? atoi(e) != 0 : true;
     }();
-    const bool relabel = circ && relabel_env && o.use_jit() && !per_gate && ctx.world == 1 && nl >= m_pad &&
-                         nl >= L + 5;
+    const bool relabel = circ && relabel_env && o.use_jit() && !per_gate && nl >= m_pad && nl >= L + 5;
     // With relabelling a smaller tile wins (tools/sweep_relabel.sh, profiles/r01_relabel_sweep.txt):
     // passes are FP-pipe bound and 4 CTAs per SM overlap their HBM phases better than 2.
     int m_def = default_tile_qubits(dbl, nl, rb);

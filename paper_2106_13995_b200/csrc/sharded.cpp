@@ -313,6 +313,14 @@ sv_status exchange_one(sv_state_s* s, int j, std::string& err) {
     return SV_OK;
 }
 
+bool shard_relabel_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SHARD_RELABEL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
 uint64_t gate_mask(const Gate& g) {
     uint64_t m = 0;
     for (int q : g.targets) m |= 1ull << q;
@@ -394,7 +402,7 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
     };
     while (!pending.empty()) {
         std::vector<std::vector<LOp>> ops(S);
-        std::vector<int> deferred;
+        std::vector<int> deferred, runnable;
         uint64_t blocked = 0;
         for (int gi : pending) {
             const Gate& gt = gates[gi];
@@ -413,8 +421,41 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
             if (needs) {
                 deferred.push_back(gi);
                 blocked |= T;
+            } else {
+                runnable.push_back(gi);
             }
         }
+        // Relabelling tile schedule for the batch (as on one GPU: passes store with a
+        // permutation of their tile qubits, fewer passes).  Planned for EVERY rank in every
+        // process -- the relabels must leave the same qubit map on all ranks (rank-constant
+        // folding can drop ops on some ranks); if any rank's map differs, the batch is
+        // planned without relabelling.  Rollouts are off here (P plans per process).
+        bool relabelled = false;
+        std::vector<Schedule> rsched(S);
+        if (shard_relabel_enabled() && o.use_jit() && !runnable.empty()) {
+            Circuit bc;
+            bc.n = n;
+            for (int gi : runnable) bc.gates.push_back(gates[gi]);
+            RunOpts o2 = o;
+            o2.no_rollout = true;
+            std::vector<Schedule> all(world);
+            std::vector<int> endp;
+            bool same = true;
+            for (int r = 0; r < world && same; ++r) {
+                std::vector<LOp> tmp;
+                const sv_status st = build_schedule(tmp, ctx_for(r), o2, all[r], err, &bc);
+                if (st != SV_OK) return st;
+                const std::vector<int> e = all[r].end_phys.empty() ? phys : all[r].end_phys;
+                if (r == 0) endp = e;
+                else same = e == endp;
+            }
+            if (same) {
+                relabelled = true;
+                for (int i = 0; i < S; ++i) rsched[i] = std::move(all[ranks[i]]);
+                phys = endp;
+            }
+        }
+        std::vector<std::vector<LOp>> swaps(S);  // pre-exchange relabel after a relabelled batch
         if (!deferred.empty()) {
             // relabel: put the g local logical qubits with the farthest next use at the top
             std::vector<long> next_use(n, (long)1 << 40);
@@ -442,7 +483,7 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
                     const int occ = logical_at[t];
                     if (inF[occ]) continue;
                     const int pq = phys[q];
-                    for (int i = 0; i < S; ++i) ops[i].push_back(phys_swap(pq, t));
+                    for (int i = 0; i < S; ++i) (relabelled ? swaps[i] : ops[i]).push_back(phys_swap(pq, t));
                     std::swap(phys[q], phys[occ]);
                     logical_at[t] = q;
                     logical_at[pq] = occ;
@@ -453,8 +494,20 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
         ShardStep batch;
         for (int i = 0; i < S; ++i) {
             Schedule sc;
-            const sv_status r = build_schedule(ops[i], ctx_for(ranks[i]), o, sc, err);
-            if (r != SV_OK) return r;
+            if (relabelled) {
+                sc = std::move(rsched[i]);
+                sc.end_phys.clear();
+                if (!swaps[i].empty()) {
+                    Schedule sw;
+                    const sv_status r = build_schedule(swaps[i], ctx_for(ranks[i]), o, sw, err);
+                    if (r != SV_OK) return r;
+                    for (PassPlan& pp : sw.passes) sc.passes.push_back(std::move(pp));
+                    sc.stages += sw.stages;
+                }
+            } else {
+                const sv_status r = build_schedule(ops[i], ctx_for(ranks[i]), o, sc, err);
+                if (r != SV_OK) return r;
+            }
             // the batch's last pass feeds the exchange: give it the remote-store variant
             if (!deferred.empty() && o.exchange == 0 && !sc.passes.empty() &&
                 sc.passes.back().kind == PassPlan::TILE && sc.passes.back().sym)
