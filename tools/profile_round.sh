@@ -13,7 +13,7 @@ ncu --metrics $M --clock-control none --csv --log-file $OUT/launches_bench_c128.
 ncu --metrics $M --clock-control none --csv --log-file $OUT/launches_mult31.csv \
     python bench.py --workload multiplier --qubits 31 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 # run_plan: 2 runs of the plan, then profiled runs; -s skips to pass p of the second run
-for spec in c64:7:p0 c64:10:p3 c128:11:p3; do
+for spec in c64:7:p0 c64:10:p3 c128:10:p3; do
   IFS=: read dt skip tag <<< "$spec"
   ncu --set full --clock-control none --import-source on -k regex:svpass -s $skip -c 1 -o /tmp/full_${dt}_$tag \
       python tools/run_plan.py --dtype $dt > /dev/null 2>&1
