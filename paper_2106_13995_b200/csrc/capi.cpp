@@ -134,7 +134,7 @@ int shard_count(const sv_state_s* s) { return s->virt ? s->world : 1; }
 int shard_rank(const sv_state_s* s, int i) { return s->virt ? i : s->rank; }
 
 sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stats* st,
-                       std::vector<cudaEvent_t>* ev = nullptr, int64_t basis = -1) {
+                       std::vector<cudaEvent_t>* ev = nullptr, int64_t basis = -1, bool uniform = false) {
     if (ev) {
         while (ev->size() < sc.passes.size() + 1) {
             cudaEvent_t x;
@@ -171,6 +171,8 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
             }
         } else if (pp.kind == PassPlan::TILE && pi == 1 && basis >= 0)
             e = jit_launch_basis(pp, psi, (uint64_t)basis, s->stream);
+        else if (pp.kind == PassPlan::TILE && pi == 1 && uniform)
+            e = jit_launch_uniform(pp, psi, uniform_amp(s->n), s->dbl, s->stream);
         else if (pp.kind == PassPlan::TILE && pp.jit_fn)
             e = jit_launch(pp, psi, s->stream);
         else if (pp.kind == PassPlan::TILE)
@@ -183,7 +185,7 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
             st->passes += 1;
             st->launches += 1;
             st->stages += pp.kind == PassPlan::TILE ? pp.nstages : 1;
-            st->hbm_bytes += (pi == 1 && basis >= 0 ? 1ull : 2ull) * pp.touched_amps * s->amp_bytes();
+            st->hbm_bytes += (pi == 1 && (basis >= 0 || uniform) ? 1ull : 2ull) * pp.touched_amps * s->amp_bytes();
         }
     }
     return SV_OK;
@@ -223,6 +225,7 @@ sv_status plan_schedule(sv_plan_s* p) {
 // Write the basis state |k> (all shards of this process).
 sv_status write_basis(sv_state_s* s, uint64_t k) {
     s->lazy_basis = -1;
+    s->lazy_uniform = false;
     const size_t shard_bytes = (size_t)s->local_amps() * s->amp_bytes();
     const int owner = (int)(k >> s->nl);
     const uint64_t local = k & (s->local_amps() - 1);
@@ -243,7 +246,19 @@ sv_status write_basis(sv_state_s* s, uint64_t k) {
 }
 
 // Write a deferred basis-state initialisation now (before anything reads the buffer).
+sv_status write_uniform(sv_state_s* s) {
+    s->lazy_basis = -1;
+    s->lazy_uniform = false;
+    const double a = uniform_amp(s->n);
+    for (int i = 0; i < shard_count(s); ++i) {
+        cudaError_t e = launch_fill(s->dbl, s->shard_ptr(i), s->local_amps(), a, 0.0, s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "fill");
+    }
+    return SV_OK;
+}
+
 sv_status materialize(sv_state_s* s) {
+    if (s->lazy_uniform) return write_uniform(s);
     if (s->lazy_basis < 0) return SV_OK;
     return write_basis(s, (uint64_t)s->lazy_basis);
 }
@@ -400,6 +415,7 @@ sv_status sv_init_basis(sv_state s, uint64_t k) {
     if (s->n < 64 && k >= (1ull << s->n)) return fail(SV_ERR_RANGE, "basis index out of range");
     for (int q = 0; q < s->n; ++q) s->phys[q] = q;
     if (s->owned && s->world == 1 && !s->virt) {
+        s->lazy_uniform = false;
         s->lazy_basis = (int64_t)k;  // written by the next plan's first pass, or by materialize()
         return SV_OK;
     }
@@ -408,14 +424,13 @@ sv_status sv_init_basis(sv_state s, uint64_t k) {
 
 sv_status sv_init_uniform(sv_state s) {
     if (!s) return fail(SV_ERR_ARG, "NULL state");
-    s->lazy_basis = -1;
     for (int q = 0; q < s->n; ++q) s->phys[q] = q;
-    const double a = uniform_amp(s->n);
-    for (int i = 0; i < shard_count(s); ++i) {
-        cudaError_t e = launch_fill(s->dbl, s->shard_ptr(i), s->local_amps(), a, 0.0, s->stream);
-        if (e != cudaSuccess) return cuda_fail(e, "fill");
+    if (s->owned && s->world == 1 && !s->virt) {
+        s->lazy_basis = -1;
+        s->lazy_uniform = true;  // synthesised by the next plan's first pass, or by materialize()
+        return SV_OK;
     }
-    return SV_OK;
+    return write_uniform(s);
 }
 
 sv_status sv_set_amplitudes(sv_state s, uint64_t first, uint64_t count, const void* host) {
@@ -597,9 +612,14 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
     }
     // fused init: a deferred basis state is synthesised by the first pass instead of written
     int64_t kb = -1;
+    bool unif = false;
     if (s->lazy_basis >= 0 && !p->opts.use_graph && !p->sched.passes.empty() && p->sched.passes[0].jit_fn_basis) {
         kb = s->lazy_basis;
         s->lazy_basis = -1;  // the map is the identity after an init
+    }
+    if (s->lazy_uniform && !p->opts.use_graph && !p->sched.passes.empty() && p->sched.passes[0].jit_fn_unif) {
+        unif = true;
+        s->lazy_uniform = false;
     }
     sv_status st = canonicalize(s);  // the plan assumes the identity layout
     if (st != SV_OK) return st;
@@ -638,7 +658,7 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
             stats->hbm_bytes = 2ull * s->local_amps() * s->amp_bytes() * tmp.passes;
         }
     } else {
-        st = run_schedule(s, s->d, p->sched, stats, p->opts.profile ? &p->prof_ev : nullptr, kb);
+        st = run_schedule(s, s->d, p->sched, stats, p->opts.profile ? &p->prof_ev : nullptr, kb, unif);
         p->prof_n = p->opts.profile ? (int)p->sched.passes.size() : 0;
     }
     if (st == SV_OK && !p->sched.end_phys.empty()) s->phys = p->sched.end_phys;  // layout-changing plan

@@ -123,6 +123,7 @@ struct PassPlan {
     std::shared_ptr<TileSym> sym;        // TILE: the symbolic pass
     void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
     void* jit_fn_basis = nullptr;        // TILE, first pass: variant whose input is a basis state
+    void* jit_fn_unif = nullptr;         // TILE, first pass: variant whose input is the uniform state
     int xS = -1;                         // TILE feeding an exchange: local bits below xS stay (f2)
     void* jit_fn_x = nullptr;            // TILE, xS >= 0: variant storing into the peers' buffers
     int jit_threads = 0;

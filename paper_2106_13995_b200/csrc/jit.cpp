@@ -800,7 +800,7 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 }  // namespace
 
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc, bool basis_in, int xS) {
+                            int& tpc, bool basis_in, int xS, bool uniform_in) {
     Em e;
     e.dbl = sym.dbl;
     const int rb = sym.rb, R = 1 << rb;
@@ -808,7 +808,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     const int tb = m - rb;
     const int tthreads = 1 << tb;  // threads per tile
     const bool multi = sym.stages.size() > 1;
-    const bool pf = !basis_in && xS < 0 && prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
+    const bool pf = !basis_in && !uniform_in && xS < 0 && prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
                     ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)tthreads == 0;
     persistent = pf;
     const size_t tile_bytes = ((size_t)1 << m) * (sym.dbl ? 16 : 8);
@@ -861,7 +861,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (xS >= 0) o << "struct XT { C* p[8]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
       << (pf ? std::max(1, min_blocks(threads, sym.dbl) / 2) : min_blocks(threads, sym.dbl)) << ") svpass(C* __restrict__ psi"
-      << (basis_in ? ",unsigned long long kb" : "") << (xS >= 0 ? ",const XT xo,unsigned xr" : "") << "){\n";
+      << (basis_in ? ",unsigned long long kb" : "") << (uniform_in ? ",const C u0" : "")
+      << (xS >= 0 ? ",const XT xo,unsigned xr" : "") << "){\n";
     if (pf) o << "extern __shared__ C sm[];\n";
     else if (multi && tpc > 1) o << "extern __shared__ C sm_[];\nC* sm=sm_+((threadIdx.x>>" << tb << ")<<" << m << ");\n";
     else if (multi) o << "extern __shared__ C sm[];\n";
@@ -1056,6 +1057,10 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             const std::string zero = sym.dbl ? "mk(0.0,0.0)" : "0ull";
             for (int s = 0; s < R; ++s)
                 o << reg(s) << "=(kb==(g|" << goff[s] << "ull))?" << one << ":" << zero << ";";
+            o << "\n";
+        } else if (!reads_smem && uniform_in) {
+            // the pass input is the uniform superposition: every amplitude is u0, read nothing
+            for (int s = 0; s < R; ++s) o << reg(s) << "=u0;";
             o << "\n";
         } else if (!reads_smem) {
             for (int s = 0; s < R; ++s) o << reg(s) << "=psi[g+" << goff[s] << "ull];";
@@ -1357,6 +1362,8 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
         int th, tpc;
         bool pers;
         srcs.back() = gen_pass_source(*first->sym, first->ntiles, th, basis_smem, pers, tpc, true);
+        size_t usm = 0;
+        srcs.push_back(gen_pass_source(*first->sym, first->ntiles, th, usm, pers, tpc, false, -1, true));
     }
     const size_t nsrc = srcs.size();
     std::vector<sv_status> st(nsrc, SV_OK);
@@ -1370,7 +1377,7 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
         pool.emplace_back([&, w]() {
             cudaSetDevice(dev);
             for (size_t i = w; i < nsrc; i += nthr)
-                st[i] = jit_compile(srcs[i], i < todo.size() ? todo[i]->jit_smem : basis_smem, &fns[i], errs[i]);
+                st[i] = jit_compile(srcs[i], i < todo.size() ? todo[i]->jit_smem : basis_smem, &fns[i], errs[i]);  // the two input variants share the pass's shared-memory size
         });
     for (auto& th : pool) th.join();
     for (size_t i = 0; i < nsrc; ++i)
@@ -1378,7 +1385,10 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
             err = errs[i];
             return st[i];
         }
-    if (first) first->jit_fn_basis = fns.back();
+    if (first) {
+        first->jit_fn_basis = fns[todo.size()];
+        first->jit_fn_unif = fns[todo.size() + 1];
+    }
     for (size_t i = 0; i < todo.size(); ++i) {
         todo[i]->jit_fn = fns[i];
         if (todo[i]->jit_persistent) {
@@ -1413,6 +1423,18 @@ cudaError_t jit_launch_x(const PassPlan& pp, void* psi, void* const outs[8], uns
     for (int i = 0; i < 8; ++i) xo.p[i] = outs[i];
     void* args[] = {&psi, &xo, &rank};
     return cudaLaunchKernel(pp.jit_fn_x, dim3(pp.jit_grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem, stream);
+}
+
+cudaError_t jit_launch_uniform(const PassPlan& pp, void* psi, double amp, bool dbl, cudaStream_t stream) {
+    struct alignas(16) C2 {
+        double x, y;
+    } u2{amp, 0.0};
+    unsigned long long u1;
+    const float f[2] = {(float)amp, 0.0f};
+    std::memcpy(&u1, f, 8);
+    void* args[] = {&psi, dbl ? (void*)&u2 : (void*)&u1};
+    return cudaLaunchKernel(pp.jit_fn_unif, dim3(pp.jit_grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem,
+                            stream);
 }
 
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {

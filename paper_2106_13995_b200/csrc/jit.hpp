@@ -8,7 +8,7 @@ namespace svb {
 
 // CUDA source of one fused tile pass; returns the launch shape.
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc, bool basis_in = false, int xS = -1);
+                            int& tpc, bool basis_in = false, int xS = -1, bool uniform_in = false);
 // Compile (or fetch from the in-process cache) and return a CUfunction.
 sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::string& err);
 // Compile every TILE pass of a schedule that has no kernel yet (parallel over passes).
@@ -17,6 +17,8 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis = false);
 cudaError_t jit_launch(const PassPlan& pp, void* psi, cudaStream_t stream);
 // first pass with the basis state |kb> as input (nothing read from psi)
 cudaError_t jit_launch_basis(const PassPlan& pp, void* psi, uint64_t kb, cudaStream_t stream);
+// first pass with the uniform superposition (every amplitude amp) as input (nothing read)
+cudaError_t jit_launch_uniform(const PassPlan& pp, void* psi, double amp, bool dbl, cudaStream_t stream);
 // fused-exchange variant (pp.xS >= 0): stores go to outs[dest rank] at the swapped index
 cudaError_t jit_launch_x(const PassPlan& pp, void* psi, void* const outs[8], unsigned rank, cudaStream_t stream);
 // whole-permutation pass (out-of-place gather)

@@ -43,6 +43,8 @@ struct sv_state_s {
     // written; the first generated tile pass of the next plan synthesises its input tile instead
     // of reading it (init fused into pass 0), anything else materialises it first.
     int64_t lazy_basis = -1;
+    // Deferred uniform superposition 2^(-n/2) (single GPU), synthesised the same way.
+    bool lazy_uniform = false;
 
     size_t amp_bytes() const { return dbl ? 16 : 8; }
     uint64_t local_amps() const { return 1ull << nl; }

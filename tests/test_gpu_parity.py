@@ -188,6 +188,31 @@ def test_merged_single_qubit_runs(P, dtype, n, seed):
         assert_close(got, ref, dtype, W.gate_count(c))
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_deferred_uniform_init(P, dtype):
+    # sv_init_uniform on one GPU is deferred: the plan's first tile pass synthesises 2^(-n/2)
+    # instead of reading (tile pass and permutation plans), any other call writes it first
+    for c in (W.supremacy(4, 4, 8, seed=5, n=16), W.multiplier(4)):
+        text = W.to_text(c)
+        nn = c.n
+        uu = np.full(1 << nn, 2.0 ** (-nn / 2), complex)
+        ref = oracle.simulate(text, uu)
+        plan = P.Plan(text, dtype)
+        with P.StateVector(nn, dtype) as sv:
+            for _ in range(2):
+                sv.init_uniform()
+                sv.apply_plan(plan)
+                assert_close(sv.amplitudes(), ref, dtype, W.gate_count(c))
+            sv.init_uniform()
+            got = sv.amplitudes()  # materialised by the readout
+            assert np.max(np.abs(got - uu)) <= (1e-7 if dtype == "c64" else 1e-15)
+            sv.init_uniform()
+            sv.apply_gate(np.array([[1, 0], [0, -1]]), [0])  # materialised before a single gate
+            z = uu.copy()
+            z[1::2] *= -1
+            assert np.max(np.abs(sv.amplitudes() - z)) <= (1e-7 if dtype == "c64" else 1e-15)
+
+
 def test_qft_20q_vs_oracle(P):
     c = W.qft(20)
     text = W.to_text(c)
