@@ -396,6 +396,53 @@ __global__ void __launch_bounds__(256) dense_k_kernel(typename V2<real>::t* __re
     }
 }
 
+// Specialised dense-k for k = 1..3 (single gates, sv_apply_gate): compile-time group size
+// (the amplitudes stay in registers), two groups in flight per thread (g and g + T, both
+// coalesced across the warp), grid sized to the SMs.
+template <typename real, int K>
+__global__ void __launch_bounds__(256) dense_kt_kernel(typename V2<real>::t* __restrict__ psi,
+                                                       const __grid_constant__ DenseParams<real> P,
+                                                       uint64_t groups) {
+    using V = typename V2<real>::t;
+    constexpr int D = 1 << K;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    auto base_of = [&](uint64_t g) {
+        uint64_t base = g;
+        for (int j = 0; j < P.nsorted; ++j) {
+            const int q = P.sorted[j];
+            base = ((base >> q) << (q + 1)) | (base & ((1ull << q) - 1));
+        }
+        return base | P.cmask;
+    };
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += 2 * T) {
+        const bool two = g + T < groups;
+        const uint64_t b0 = base_of(g), b1 = two ? base_of(g + T) : b0;
+        V x[D], y[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[c] = psi[b0 + P.off[c]];
+        if (two) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) y[c] = psi[b1 + P.off[c]];
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            V acc = cmul(x[0], P.M[2 * (r * D)], P.M[2 * (r * D) + 1]);
+#pragma unroll
+            for (int c = 1; c < D; ++c) acc = cfma(acc, x[c], P.M[2 * (r * D + c)], P.M[2 * (r * D + c) + 1]);
+            psi[b0 + P.off[r]] = acc;
+        }
+        if (two) {
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                V acc = cmul(y[0], P.M[2 * (r * D)], P.M[2 * (r * D) + 1]);
+#pragma unroll
+                for (int c = 1; c < D; ++c) acc = cfma(acc, y[c], P.M[2 * (r * D + c)], P.M[2 * (r * D + c) + 1]);
+                psi[b1 + P.off[r]] = acc;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ init (K1)
 template <typename real>
 __global__ void fill_kernel(typename V2<real>::t* __restrict__ psi, uint64_t N, real re, real im) {
@@ -615,8 +662,30 @@ static unsigned grid_for(uint64_t work, int threads) {
     return (unsigned)(b < cap ? (b ? b : 1) : cap);
 }
 
+template <typename real>
+static void launch_dense_kt(int k, typename V2<real>::t* psi, const DenseParams<real>& P, uint64_t groups,
+                            unsigned grid, cudaStream_t st) {
+    if (k == 1) dense_kt_kernel<real, 1><<<grid, 256, 0, st>>>(psi, P, groups);
+    else if (k == 2) dense_kt_kernel<real, 2><<<grid, 256, 0, st>>>(psi, P, groups);
+    else dense_kt_kernel<real, 3><<<grid, 256, 0, st>>>(psi, P, groups);
+}
+
 cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t groups, cudaStream_t st) {
     const int threads = 256;
+    const int k = dbl ? reinterpret_cast<const DenseParams<double>*>(params)->k
+                      : reinterpret_cast<const DenseParams<float>*>(params)->k;
+    if (k <= 3) {
+        // persistent-ish grid: 8 blocks of 256 per SM, each thread two groups per iteration
+        const uint64_t want = (groups + 2 * threads - 1) / (2 * threads);
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 8));
+        if (dbl)
+            launch_dense_kt<double>(k, reinterpret_cast<double2*>(psi), *reinterpret_cast<const DenseParams<double>*>(params),
+                                    groups, grid, st);
+        else
+            launch_dense_kt<float>(k, reinterpret_cast<float2*>(psi), *reinterpret_cast<const DenseParams<float>*>(params),
+                                   groups, grid, st);
+        return cudaGetLastError();
+    }
     if (dbl)
         dense_k_kernel<double><<<grid_for(groups, threads), threads, 0, st>>>(
             reinterpret_cast<double2*>(psi), *reinterpret_cast<const DenseParams<double>*>(params), groups);
