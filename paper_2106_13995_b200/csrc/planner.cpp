@@ -689,6 +689,16 @@ bool diag_into_regs() {
     return b;
 }
 
+bool balance_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_BALANCE");
+        // measured (profiles/r01_balance.txt): 30 q supremacy c64 24.2 -> 24.7 ms, c128 7 -> 8
+        // passes -- the greedy fullest passes win; off by default
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
 int rollout_k() {
     static int k = [] {
         const char* e = getenv("SV_ROLLOUT");
@@ -777,13 +787,14 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
     };
     // choose the pass's gates and tile qubits, starting from tile qubits S0; `order` records
     // the order in which qubits joined the tile
+    double cur_budget = -1;  // > 0: this pass's cost cap (balance search below)
     auto select = [&](const std::vector<int>& rem, uint64_t S0, std::vector<int>& pass_ops, std::vector<int>& deferred,
                       std::vector<int>* order) -> uint64_t {
         uint64_t S = S0;
         Blocker blocked;
         size_t ncoef = 0;
         double cost = 0;
-        const double budget = o.use_jit() ? pass_budget() : 1e30;
+        const double budget = cur_budget > 0 ? cur_budget : o.use_jit() ? pass_budget() : 1e30;
         for (int idx : rem) {
             const LOp& op = ops[idx];
             const bool full = per_gate ? !pass_ops.empty()
@@ -827,6 +838,112 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             continue;
         }
         uint64_t S = select(remaining, lowmask, pass_ops, deferred, nullptr);
+        // Balance search (SV_BALANCE): a pass whose FP work exceeds its HBM time leaves the
+        // memory system idle while lighter passes later leave the FP pipe idle.  Try capping
+        // this pass's op cost (90/80/70 % of the greedy pass), plan the rest greedily, and keep
+        // the cap that minimises the modelled time sum_p max(cost_p, H_p) (H_p: the op cost the
+        // FP pipe retires in one pass's HBM time, ~87 units at 2 x 2^n x b bytes, half for a
+        // first pass that only writes; tools/sass_stats.py + per-pass times).
+        if (relabel && !o.no_rollout && balance_enabled() && !pass_ops.empty()) {
+            auto pass_cost = [&](const std::vector<int>& po) {
+                double c = 0;
+                for (int idx : po) c += op_cost(ops[idx]);
+                return c;
+            };
+            const double Hfull = 87.0;
+            const double H0 = out.passes.empty() ? Hfull / 2 : Hfull;
+            auto model = [&](double budget_cap, double& obj, size_t& npass) -> bool {
+                std::vector<int> po, de;
+                cur_budget = budget_cap;
+                const uint64_t S2 = select(remaining, lowmask, po, de, nullptr);
+                cur_budget = -1;
+                if (po.empty()) return false;
+                obj = std::max(pass_cost(po), H0);
+                npass = 1;
+                if (de.empty()) return true;
+                // this pass's relabel as the real planner would pick it (1-step score)
+                Context c2 = ctx;
+                {
+                    std::vector<int> tq2;
+                    for (int q = 0; q < 64; ++q)
+                        if ((S2 >> q) & 1) tq2.push_back(q);
+                    const int nt2 = (int)tq2.size();
+                    double bs = -1;
+                    uint64_t bm = lowmask;
+                    if (nt2 <= 20 && nt2 >= L) {
+                        uint32_t c = (1u << L) - 1;
+                        while (c < (1u << nt2)) {
+                            uint64_t low = 0;
+                            for (int j = 0; j < nt2; ++j)
+                                if ((c >> j) & 1) low |= 1ull << tq2[j];
+                            std::vector<int> pn, dn;
+                            select(de, low, pn, dn, nullptr);
+                            double sc = pass_cost(pn) + (dn.empty() ? 1e6 : 0) + 1e-6 * popc(low & lowmask);
+                            if (sc > bs) { bs = sc; bm = low; }
+                            const uint32_t u = c & (0u - c), w = c + u;
+                            c = w | (((w ^ c) >> 2) / u);
+                        }
+                    }
+                    std::vector<int> pm(64), free_slots, ls;
+                    for (int q = 0; q < 64; ++q) pm[q] = q;
+                    for (int q = 0; q < 64; ++q)
+                        if ((bm >> q) & 1) ls.push_back(q);
+                    for (int slot = 0; slot < L; ++slot)
+                        if (std::find(ls.begin(), ls.end(), slot) == ls.end()) free_slots.push_back(slot);
+                    size_t fi = 0;
+                    for (int q : ls) {
+                        if (q < L) continue;
+                        pm[q] = free_slots[fi];
+                        pm[free_slots[fi++]] = q;
+                    }
+                    for (int& p : c2.phys) p = pm[p];
+                }
+                Circuit sub;
+                sub.n = circ->n;
+                std::vector<int> g2;
+                for (int idx : de) g2.push_back(ops[idx].gate);
+                std::sort(g2.begin(), g2.end());
+                g2.erase(std::unique(g2.begin(), g2.end()), g2.end());
+                for (int gi : g2) sub.gates.push_back(circ->gates[gi]);
+                RunOpts o2 = o;
+                o2.no_rollout = true;
+                Schedule s2;
+                std::vector<LOp> ops2;
+                std::string e2;
+                if (build_schedule(ops2, c2, o2, s2, e2, &sub) != SV_OK) return false;
+                npass += s2.passes.size();
+                for (const PassPlan& pp : s2.passes) {
+                    double c = 0;
+                    if (pp.sym)
+                        for (const StageSym& st : pp.sym->stages)
+                            for (const LOp& op : st.ops) c += op_cost(op);
+                    obj += std::max(c, Hfull);
+                }
+                return true;
+            };
+            const double c0 = pass_cost(pass_ops);
+            double best_obj;
+            size_t np0 = 0;
+            if (c0 > H0 && model(1e30, best_obj, np0)) {
+                double best_cap = -1;
+                for (double f : {0.9, 0.8, 0.7}) {
+                    double ob;
+                    size_t np;
+                    // never trade an extra pass (a full HBM round trip) for balance
+                    if (model(f * c0, ob, np) && np <= np0 && ob < best_obj - 1e-9) {
+                        best_obj = ob;
+                        best_cap = f * c0;
+                    }
+                }
+                if (best_cap > 0) {
+                    pass_ops.clear();
+                    deferred.clear();
+                    cur_budget = best_cap;
+                    S = select(remaining, lowmask, pass_ops, deferred, nullptr);
+                    cur_budget = -1;
+                }
+            }
+        }
         // Register bits of this pass: a heavy pass takes one fewer (half the code per op): its
         // straight-line kernel otherwise outgrows the instruction cache and stalls on fetch
         // (profiles/r01_icache.txt: 50% no_instructions at ~4000 instructions).
