@@ -457,10 +457,11 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": args.dtype,
+            "dtype": "f64" if args.dtype == "c128" else "f32",  # arithmetic type (complex64 state: FP32)
             "data": "synthetic",
             "config": {
                 "workload": name,
+                "state_dtype": "complex128" if args.dtype == "c128" else "complex64",
                 "n_qubits": n,
                 "n_qubits_per_gpu": n - (world.bit_length() - 1),
                 "gates": G,
