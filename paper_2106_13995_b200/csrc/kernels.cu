@@ -443,6 +443,62 @@ __global__ void __launch_bounds__(256) dense_kt_kernel(typename V2<real>::t* __r
     }
 }
 
+// complex64 dense-k with qubit 0 free (no gate qubit on it): groups 2h and 2h+1 have bases
+// b and b+1, so one 16-byte load fetches the same matrix index of both groups; two such
+// group pairs in flight per thread.
+template <int K>
+__global__ void __launch_bounds__(256) dense_kv_kernel(float4* __restrict__ psi4,
+                                                       const __grid_constant__ DenseParams<float> P,
+                                                       uint64_t pairs) {
+    constexpr int D = 1 << K;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    auto base_of = [&](uint64_t g) {  // g = even group index
+        uint64_t base = g;
+        for (int j = 0; j < P.nsorted; ++j) {
+            const int q = P.sorted[j];
+            base = ((base >> q) << (q + 1)) | (base & ((1ull << q) - 1));
+        }
+        return (base | P.cmask) >> 1;  // in float4 units
+    };
+    auto apply = [&](float4 (&x)[D]) {
+        float4 y[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            float ar = 0.f, ai = 0.f, br = 0.f, bi = 0.f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const float mr = P.M[2 * (r * D + c)], mi = P.M[2 * (r * D + c) + 1];
+                ar = fmaf(x[c].x, mr, fmaf(-x[c].y, mi, ar));
+                ai = fmaf(x[c].x, mi, fmaf(x[c].y, mr, ai));
+                br = fmaf(x[c].z, mr, fmaf(-x[c].w, mi, br));
+                bi = fmaf(x[c].z, mi, fmaf(x[c].w, mr, bi));
+            }
+            y[r] = make_float4(ar, ai, br, bi);
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) x[r] = y[r];
+    };
+    for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < pairs; h += 2 * T) {
+        const bool two = h + T < pairs;
+        const uint64_t b0 = base_of(2 * h), b1 = two ? base_of(2 * (h + T)) : b0;
+        float4 x[D], z[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[c] = psi4[b0 + (P.off[c] >> 1)];
+        if (two) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) z[c] = psi4[b1 + (P.off[c] >> 1)];
+        }
+        apply(x);
+#pragma unroll
+        for (int r = 0; r < D; ++r) psi4[b0 + (P.off[r] >> 1)] = x[r];
+        if (two) {
+            apply(z);
+#pragma unroll
+            for (int r = 0; r < D; ++r) psi4[b1 + (P.off[r] >> 1)] = z[r];
+        }
+    }
+}
+
 // ------------------------------------------------------------------ init (K1)
 template <typename real>
 __global__ void fill_kernel(typename V2<real>::t* __restrict__ psi, uint64_t N, real re, real im) {
@@ -678,12 +734,24 @@ cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t gro
         // persistent-ish grid: 8 blocks of 256 per SM, each thread two groups per iteration
         const uint64_t want = (groups + 2 * threads - 1) / (2 * threads);
         const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 8));
-        if (dbl)
+        if (dbl) {
             launch_dense_kt<double>(k, reinterpret_cast<double2*>(psi), *reinterpret_cast<const DenseParams<double>*>(params),
                                     groups, grid, st);
-        else
-            launch_dense_kt<float>(k, reinterpret_cast<float2*>(psi), *reinterpret_cast<const DenseParams<float>*>(params),
-                                   groups, grid, st);
+        } else {
+            const auto& P = *reinterpret_cast<const DenseParams<float>*>(params);
+            if (P.nsorted > 0 && P.sorted[0] >= 1 && groups >= 2) {
+                // qubit 0 free: 16-byte loads over group pairs
+                const uint64_t pairs = groups / 2;
+                const uint64_t w2 = (pairs + 2 * threads - 1) / (2 * threads);
+                const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(w2, 148ull * 8));
+                float4* p4 = reinterpret_cast<float4*>(psi);
+                if (k == 1) dense_kv_kernel<1><<<g2, threads, 0, st>>>(p4, P, pairs);
+                else if (k == 2) dense_kv_kernel<2><<<g2, threads, 0, st>>>(p4, P, pairs);
+                else dense_kv_kernel<3><<<g2, threads, 0, st>>>(p4, P, pairs);
+            } else {
+                launch_dense_kt<float>(k, reinterpret_cast<float2*>(psi), P, groups, grid, st);
+            }
+        }
         return cudaGetLastError();
     }
     if (dbl)
