@@ -7,7 +7,7 @@ OUT=profiles
   echo "# python bench.py --steps 2 --warmup 3 (30q supremacy d20 c64), B200; per-launch times are serialised/cold"
   python tools/ncu_summary.py launches $IN/launches_bench_c64.csv; } > $OUT/${R}_launches_bench_c64.txt
 { echo "# same, --dtype c128"; python tools/ncu_summary.py launches $IN/launches_bench_c128.csv; } > $OUT/${R}_launches_bench_c128.txt
-{ echo "# same, --workload multiplier --qubits 31 (8x7, uniform input: fill + relabel pass + gather pass per step)"
+{ echo "# same, --workload multiplier --qubits 31 (8x7, uniform input synthesised by the relabel pass, then the gather pass)"
   python tools/ncu_summary.py launches $IN/launches_mult31.csv; } > $OUT/${R}_launches_mult31.txt
 for spec in c64_p0 c64_p3 c128_p3; do
   { echo "# ncu --set full --clock-control none, 30q supremacy d20 plan, ${spec%%_*} tile pass ${spec##*_p}, B200"
