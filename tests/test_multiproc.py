@@ -78,3 +78,17 @@ def test_shard_plan_random_and_multiplier():
             assert info["batches"] == info["swaps"] + 1
     with pytest.raises(P.SvError):
         P.Plan("qubits: 4\nH 0\n").shard_info(3)
+
+
+def test_planner_pass_counts_regression():
+    """Host planner regression pins (measured plans of DESIGN.md 6.1 / 7): the 30 q supremacy
+    d20 circuit in 7 passes for both dtypes (relabelling + rollout), and the weak-scaling
+    shards with relabelled batches (31 q / P = 2: 8 passes per shard, 33 q / P = 8: 10)."""
+    import paper_2106_13995_b200 as P
+    text = W.to_text(W.supremacy(6, 5, 20, seed=0))
+    assert P.Plan(text, "c64").info()["passes"] <= 7
+    assert P.Plan(text, "c128").info()["passes"] <= 7
+    for n, world, most in [(31, 2, 8), (33, 8, 10)]:
+        t = W.to_text(W.supremacy((n + 4) // 5, 5, 20, seed=0, n=n))
+        info = P.Plan(t, "c64").shard_info(world)
+        assert info["swaps"] == 1 and info["passes"] <= most, (n, world, info)
