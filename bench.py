@@ -419,6 +419,26 @@ def run_ours(args):
         roofline["alu"] = alu_roof
         roofline["floor_frac"] = max(t_hbm, t_alu) * 1e3 / avg_launch_ms
 
+    # Per-pass breakdown (single GPU, outside the timed region): the same plan compiled with
+    # per-pass CUDA events, three back-to-back runs; each pass's algorithmic HBM bytes (2 x
+    # state, 1 x for a first pass that synthesises its input) over its own duration.
+    if world == 1:
+        try:
+            pplan = P.Plan(text, args.dtype, profile=True)
+            for _ in range(3):
+                init()
+                pst = sv.apply_plan(pplan)
+            pt = pplan.pass_times()
+            state_b = local_amps * amp
+            per = []
+            for i, ms in enumerate(pt):
+                b = state_b * (1 if i == 0 and pst["hbm_bytes"] < 2 * state_b * len(pt) else 2)
+                per.append({"ms": round(ms, 4), "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 3)})
+            roofline["per_pass"] = per
+            pplan.close()
+        except Exception as e:  # report, never hide
+            roofline["per_pass"] = f"unavailable: {e}"
+
     # e2e: same metric through the public API with host buffers: IR text in, parse + plan +
     # init + apply, marginal probabilities of 20 qubits (8 MiB fp64) back to the host.
     e2e_q = list(range(min(20, n)))
