@@ -542,7 +542,12 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     size_t smem;
     bool pers;
     int tpc;
-    if (pp.kind == PassPlan::TILE && pp.sym) src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers, tpc);
+    if (pp.kind == PassPlan::TILE && pp.sym) {
+        jit_carries(p->sched);
+        cd out;
+        src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers, tpc, false, -1, false, pp.carry_in,
+                              pp.carry_next ? &out : nullptr);
+    }
     else if (pp.kind == PassPlan::PERM) src = gen_perm_source(pp, pp.perm_dbl, threads);
     if (len) *len = src.size();
     if (buf && cap) {

@@ -124,6 +124,8 @@ struct PassPlan {
     void* jit_fn = nullptr;              // TILE: specialised kernel (CUfunction), or null = interpreter
     void* jit_fn_basis = nullptr;        // TILE, first pass: variant whose input is a basis state
     void* jit_fn_unif = nullptr;         // TILE, first pass: variant whose input is the uniform state
+    cd carry_in = 1;                     // TILE: global phase left pending by the previous pass
+    bool carry_next = false;             // TILE: leaves its non-unit global phase to the next pass
     int xS = -1;                         // TILE feeding an exchange: local bits below xS stay (f2)
     void* jit_fn_x = nullptr;            // TILE, xS >= 0: variant storing into the peers' buffers
     int jit_threads = 0;

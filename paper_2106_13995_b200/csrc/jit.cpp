@@ -800,7 +800,7 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 }  // namespace
 
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc, bool basis_in, int xS, bool uniform_in) {
+                            int& tpc, bool basis_in, int xS, bool uniform_in, cd carry_in, cd* carry_out) {
     Em e;
     e.dbl = sym.dbl;
     const int rb = sym.rb, R = 1 << rb;
@@ -918,6 +918,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     }
     const std::string SM = pf ? "bc" : "sm";
     PassState ps;
+    ps.fac = carry_in;  // global phase left pending by the previous pass of the schedule
     ps.ph.assign(R, cd(1, 0));
     ps.rs.assign(R, std::string());
     // thread-bit order of every stage: thread bit i <-> tile qubit tq_phys[i] (local position
@@ -1121,6 +1122,21 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             if (!rscale.empty())
                 for (int s = 0; s < R; ++s) ps.rs[s] = sign_mul(e, ps, ps.rs[s], rscale);
             o << "// deferred factors of the pass (scalar, per register qubit, per register)\n";
+            // A global phase that is not +-1, +-i (e.g. the e^{i pi/4} of SqrtX/SqrtY) would cost
+            // a full complex multiply per amplitude; when another generated pass follows in the
+            // schedule it is left pending for that pass (a global phase commutes with every
+            // gate) and only the magnitudes are applied here.
+            if (carry_out) {
+                *carry_out = 1;
+                const double mag = std::abs(ps.fac);
+                if (mag > 0) {
+                    const cd u = ps.fac / mag;
+                    if (!is_unit(u) && !is1(u)) {
+                        *carry_out = u;
+                        ps.fac = mag;
+                    }
+                }
+            }
             for (int s = 0; s < R; ++s) {
                 cd c = ps.fac;
                 for (auto& kv : ps.pend) c *= ((s >> sc.pos[kv.first]) & 1) ? kv.second.second : kv.second.first;
@@ -1316,6 +1332,44 @@ std::string gen_perm_source(const PassPlan& pp, bool dbl, int& threads) {
     return o.str();
 }
 
+bool carry_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_PHASE_CARRY");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
+// Global-phase carries along a schedule: a generated tile pass followed by another one leaves
+// its non-unit global phase to it (gen_pass_source); computed in pass order.
+void jit_carries(Schedule& sc) {
+    {
+        cd carry = 1;
+        for (size_t pi = 0; pi < sc.passes.size(); ++pi) {
+            PassPlan& pp = sc.passes[pi];
+            const bool gen = pp.kind == PassPlan::TILE && pp.sym;
+            if (!gen) {
+                carry = 1;
+                continue;
+            }
+            const bool next_gen = pi + 1 < sc.passes.size() && sc.passes[pi + 1].kind == PassPlan::TILE &&
+                                  sc.passes[pi + 1].sym && carry_enabled();
+            pp.carry_in = carry;
+            pp.carry_next = next_gen;
+            if (!next_gen) {
+                carry = 1;
+                continue;
+            }
+            int th, tpc;
+            size_t sm;
+            bool pers;
+            cd out = 1;
+            gen_pass_source(*pp.sym, pp.ntiles, th, sm, pers, tpc, false, -1, false, pp.carry_in, &out);
+            carry = out;
+        }
+    }
+}
+
 // fused-exchange variants of the passes that feed a global<->local swap
 static sv_status jit_prepare_x(Schedule& sc, std::string& err) {
     for (PassPlan& pp : sc.passes) {
@@ -1323,7 +1377,9 @@ static sv_status jit_prepare_x(Schedule& sc, std::string& err) {
         int th, tpc;
         size_t sm;
         bool pers;
-        const std::string src = gen_pass_source(*pp.sym, pp.ntiles, th, sm, pers, tpc, false, pp.xS);
+        cd out;
+        const std::string src = gen_pass_source(*pp.sym, pp.ntiles, th, sm, pers, tpc, false, pp.xS, false,
+                                                pp.carry_in, pp.carry_next ? &out : nullptr);
         const sv_status r = jit_compile(src, sm, &pp.jit_fn_x, err);
         if (r != SV_OK) return r;
     }
@@ -1341,6 +1397,7 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
                           : nullptr;
     if (todo.empty() && !first) return jit_prepare_x(sc, err);
     std::vector<std::string> srcs(todo.size() + (first ? 1 : 0));
+    jit_carries(sc);
     for (size_t i = 0; i < todo.size(); ++i) {
         if (todo[i]->kind == PassPlan::PERM) {
             srcs[i] = gen_perm_source(*todo[i], todo[i]->perm_dbl, todo[i]->jit_threads);
@@ -1348,8 +1405,10 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
             todo[i]->ntiles = ((1ull << todo[i]->m) >> 5) / (uint64_t)todo[i]->jit_threads;
         } else {
             int tpc = 1;
+            cd out;
             srcs[i] = gen_pass_source(*todo[i]->sym, todo[i]->ntiles, todo[i]->jit_threads, todo[i]->jit_smem,
-                                      todo[i]->jit_persistent, tpc);
+                                      todo[i]->jit_persistent, tpc, false, -1, false, todo[i]->carry_in,
+                                      todo[i]->carry_next ? &out : nullptr);
             todo[i]->jit_grid = (unsigned)(todo[i]->ntiles / (uint64_t)tpc);
         }
     }
@@ -1361,9 +1420,12 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
     if (first) {
         int th, tpc;
         bool pers;
-        srcs.back() = gen_pass_source(*first->sym, first->ntiles, th, basis_smem, pers, tpc, true);
+        cd o1, o2;
+        srcs.back() = gen_pass_source(*first->sym, first->ntiles, th, basis_smem, pers, tpc, true, -1, false,
+                                      first->carry_in, first->carry_next ? &o1 : nullptr);
         size_t usm = 0;
-        srcs.push_back(gen_pass_source(*first->sym, first->ntiles, th, usm, pers, tpc, false, -1, true));
+        srcs.push_back(gen_pass_source(*first->sym, first->ntiles, th, usm, pers, tpc, false, -1, true,
+                                       first->carry_in, first->carry_next ? &o2 : nullptr));
     }
     const size_t nsrc = srcs.size();
     std::vector<sv_status> st(nsrc, SV_OK);

@@ -8,7 +8,10 @@ namespace svb {
 
 // CUDA source of one fused tile pass; returns the launch shape.
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc, bool basis_in = false, int xS = -1, bool uniform_in = false);
+                            int& tpc, bool basis_in = false, int xS = -1, bool uniform_in = false,
+                            cd carry_in = 1, cd* carry_out = nullptr);
+// Global-phase carries of a schedule (PassPlan::carry_in / carry_next), in pass order.
+void jit_carries(Schedule& sc);
 // Compile (or fetch from the in-process cache) and return a CUfunction.
 sv_status jit_compile(const std::string& src, size_t smem, void** fn_out, std::string& err);
 // Compile every TILE pass of a schedule that has no kernel yet (parallel over passes).
