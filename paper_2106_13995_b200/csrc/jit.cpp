@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <set>
 #include <map>
 #include <mutex>
 #include <algorithm>
@@ -36,6 +37,7 @@ struct Em {
     std::ostringstream o;
     bool dbl = false;
     std::map<std::string, std::string> rk;  // per-thread run-time constants already declared
+    std::set<std::string> pure_signs;       // run-time values that are exactly +-1
     int nvar = 0;
 
     std::string lit(double v) const {
@@ -157,12 +159,29 @@ std::pair<std::string, std::string> mul_rt(Em& e, const std::string& v, const cd
 }
 
 // acc + c * r * v with a run-time sign r (empty r: f2_term)
+bool sign_xor() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SIGN_XOR");
+        // measured (profiles/r01_sign_xor.txt): 30 q supremacy c64 23.9 -> 25.4 ms -- the
+        // integer XORs and the extra registers cost more issue slots than the slower FFMA2
+        // form saves on the FMA pipe; off by default
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
 std::string f2_term_rt(Em& e, const std::string& acc, const std::string& v, const cd& c, const std::string& r) {
     if (r.empty()) return f2_term(acc, v, c);
     const double cr = c.real(), ci = c.imag();
     auto fm = [&](const std::string& u, const std::string& k) {
         return acc.empty() ? "M(" + u + "," + k + ")" : "F(" + u + "," + k + "," + acc + ")";
     };
+    // a term with a run-time sign (+-1 per thread): flip the sign bits with an integer XOR
+    // (ALU pipe) and keep the compile-time coefficient as an immediate / operand modifier
+    // (FADD2 / FFMA2-imm, 2 cycles) instead of an FFMA2 / FMUL2 with a register multiplier
+    // (3 / 2 cycles on the FMA pipe, profiles/r01_fp_rate.txt); the signs are +-1.0 pairs,
+    // so their sign bits are the mask
+    if (!e.dbl && sign_xor() && e.pure_signs.count(r)) return f2_term(acc, "SX(" + v + "," + r + ")", c);
     if (ci == 0.0 && std::abs(cr) == 1.0) return fm(cr > 0 ? v : "N(" + v + ")", r);
     if (cr == 0.0 && std::abs(ci) == 1.0) return fm(ci > 0 ? "I(" + v + ")" : "NI(" + v + ")", r);
     if (ci == 0.0) return fm(v, rt_const(e, cr, r));
@@ -236,6 +255,7 @@ std::string make_sign(Em& e, const std::string& cond, double c_true, double c_fa
     const std::string name = "sg" + std::to_string(e.nvar++);
     if (e.dbl) e.o << "const R " << name << "=(" << cond << ")?" << e.lit(c_true) << ":" << e.lit(c_false) << ";";
     else e.o << "const C " << name << "=(" << cond << ")?" << k2(c_true, c_true) << ":" << k2(c_false, c_false) << ";";
+    if (std::abs(c_true) == 1.0 && std::abs(c_false) == 1.0) e.pure_signs.insert(name);
     return name;
 }
 
@@ -250,6 +270,7 @@ std::string sign_mul(Em& e, PassState& ps, const std::string& a, const std::stri
         const std::string name = "sg" + std::to_string(e.nvar++);
         if (e.dbl) e.o << "const R " << name << "=" << a << "*" << b << ";";
         else e.o << "const C " << name << "=M(" << a << "," << b << ");";
+        if (e.pure_signs.count(a) && e.pure_signs.count(b)) e.pure_signs.insert(name);
         it = ps.sgprod.emplace(key, name).first;
     }
     return it->second;
@@ -844,6 +865,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
              "DI C N(C a){return pk(-lo(a),-hi(a));}\n"
              "DI C I(C a){return pk(-hi(a),lo(a));}\n"
              "DI C NI(C a){return pk(hi(a),-lo(a));}\n"
+             "DI C SX(C a,C s){return a^(s&0x8000000080000000ull);}\n"
              "DI C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}\n";
         // FFMA2 issues at 1/3 per cycle on B200, two scalar FFMAs at 1 each
         // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes

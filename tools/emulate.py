@@ -40,6 +40,7 @@ static inline C F1(C a,C b,C c){return pk(std::fmaf(lo(a),lo(b),lo(c)),std::fmaf
 static inline C N(C a){return pk(-lo(a),-hi(a));}
 static inline C I(C a){return pk(-hi(a),lo(a));}
 static inline C NI(C a){return pk(hi(a),-lo(a));}
+static inline C SX(C a,C s){return a^(s&0x8000000080000000ull);}
 static inline C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}
 """
 
