@@ -675,8 +675,10 @@ double heavy_pass_cost(bool dbl) {
     }();
     static double b2 = [] {
         const char* e = getenv("SV_HEAVY_COST128");
-        // c128: 52.7 ms at 200, 52.6 at 160, 54.6 at 130, 57.4 at 100
-        return e ? atof(e) : 160.0;
+        // c128: 52.7 ms at 200, 52.6 at 160, 54.6 at 130, 57.4 at 100 (8-pass plan); with the
+        // 7-pass rollout plan 130 wins in every repeat: 46.1/45.8/.. vs 46.6/46.9/.. at 160
+        // (profiles/r01_heavy_sweep.txt)
+        return e ? atof(e) : 130.0;
     }();
     return dbl ? b2 : b;
 }
