@@ -676,9 +676,9 @@ double heavy_pass_cost(bool dbl) {
     static double b2 = [] {
         const char* e = getenv("SV_HEAVY_COST128");
         // c128: 52.7 ms at 200, 52.6 at 160, 54.6 at 130, 57.4 at 100 (8-pass plan); with the
-        // 7-pass rollout plan 130 wins in every repeat: 46.1/45.8/.. vs 46.6/46.9/.. at 160
-        // (profiles/r01_heavy_sweep.txt)
-        return e ? atof(e) : 130.0;
+        // 7-pass rollout plan 130 and 160 are within run-to-run noise (three repeats each:
+        // 45.8-46.9 vs 45.8-47.1 ms, profiles/r01_heavy_sweep.txt)
+        return e ? atof(e) : 160.0;
     }();
     return dbl ? b2 : b;
 }
