@@ -125,9 +125,10 @@ sv_status sv_create_virtual_sharded(int n, sv_dtype dtype, int world, void* stre
 
 sv_status sv_destroy(sv_state s);
 
-/* Basis-state initialisation.  On a single-GPU state that owns its buffer the write is
- * deferred: the next sv_plan_apply / sv_apply_circuit whose first pass is a generated tile
- * pass synthesises |k> inside that pass (init fused into pass 0, no read of the buffer);
+/* Initialisation (basis state, or the uniform superposition).  On a single-GPU state that
+ * owns its buffer the write is deferred: the next sv_plan_apply / sv_apply_circuit whose
+ * first pass is a generated tile pass synthesises |k> (or 2^(-n/2) everywhere) inside that
+ * pass (init fused into pass 0, no read of the buffer);
  * every other call (readouts, sv_apply_gate, sv_sync, sv_device_ptr, ...) writes it first.
  * Code that reads the buffer through a pointer obtained earlier calls sv_sync first. */
 sv_status sv_init_zero(sv_state s);
