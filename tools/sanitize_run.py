@@ -1,6 +1,7 @@
 """Small run touching every kernel family, for compute-sanitizer (memcheck / racecheck /
 synccheck): generated multi-stage tile passes (c64, c128), interpreter and dense-k kernels,
 the gather pass with its relabel pass, marginal / norm readout, virtual-sharded exchanges.
+Round-1 additions: fused / peer-copy exchange, dense-k single gates, deferred uniform input.
 Checks results against the oracle so a silent corruption also fails."""
 import os
 import sys
@@ -43,4 +44,33 @@ with P.StateVector.virtual_sharded(12, 4, "c128") as sv:
     sv.set_amplitudes(psi0)
     sv.apply_circuit(rt)
     check(sv.amplitudes(), oracle.simulate(rt, psi0), 1e-11)
+# this round's additions: fused peer-memory exchange (remote-store pass variants) and the
+# peer-copy kernel after interpreter passes, c64 and c128, P = 2 and 8
+for dt, tol in (("c64", 1e-5), ("c128", 1e-12)):
+    for world in (2, 8):
+        for opts in ({}, {"fuse": False}):
+            with P.StateVector.virtual_sharded(16, world, dt) as sv:
+                st = sv.apply_circuit(t, **opts)
+                assert st["swaps"] >= 1
+                check(sv.amplitudes(), ref, tol)
+# single gates through the dense-k kernels (k = 1..3, with/without controls, qubit 0 free or not)
+h = 2 ** -0.5
+u2 = np.linalg.qr(np.random.default_rng(1).normal(size=(4, 4)) + 0j)[0]
+u3 = np.linalg.qr(np.random.default_rng(2).normal(size=(8, 8)) + 0j)[0]
+for dt, tol in (("c64", 1e-5), ("c128", 1e-12)):
+    psi0 = W.random_state(14, 5)
+    ref2 = psi0.copy()
+    with P.StateVector(14, dt) as sv:
+        sv.set_amplitudes(psi0)
+        for U, tg, ct in ((np.array([[h, h], [h, -h]]), [0], []), (np.array([[h, h], [h, -h]]), [9], [0]),
+                          (u2, [3, 11], []), (u2, [1, 0], [13]), (u3, [2, 7, 12], []), (u3, [4, 5, 6], [0, 1])):
+            sv.apply_gate(U, tg, ct)
+            ref2 = oracle.apply_gate(ref2, U, tg, ct)
+        check(sv.amplitudes(), ref2, tol if dt == "c128" else 1e-5)
+# deferred uniform input synthesised by the first pass; merged unit-class runs
+for dt, tol in (("c64", 1e-5), ("c128", 1e-12)):
+    with P.StateVector(16, dt) as sv:
+        sv.init_uniform()
+        sv.apply_circuit(t)
+        check(sv.amplitudes(), oracle.simulate(t, np.full(1 << 16, 2.0 ** -8, complex)), tol)
 print("sanitize run ok")
