@@ -701,6 +701,17 @@ bool balance_enabled() {
     return b;
 }
 
+// Rollout tie-break by the modelled time (SV_ROLLOUT_BALANCE; default: complex64 only).
+// Measured (profiles/r01_rollout.txt): c64 30 q supremacy 24.08-24.12 -> 23.92 ms (same 7
+// passes, lighter heavy passes); c128: the balanced choice ends in 8 passes instead of 7.
+bool rollout_balance(bool dbl) {
+    static const int b = [] {
+        const char* e = getenv("SV_ROLLOUT_BALANCE");
+        return e ? atoi(e) : -1;
+    }();
+    return b < 0 ? !dbl : b != 0;
+}
+
 int rollout_k() {
     static int k = [] {
         const char* e = getenv("SV_ROLLOUT");
@@ -1154,6 +1165,8 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                 RunOpts o2 = o;
                 o2.no_rollout = true;
                 size_t best_passes = SIZE_MAX;
+                double best_model = 1e300;
+                const bool tie_model = rollout_balance(dbl);
                 for (int k = 0; k < K && k < (int)cands.size(); ++k) {
                     std::vector<int> ls;
                     const std::vector<int> pm = perm_for(cands[k].second, ls);
@@ -1164,8 +1177,21 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                     std::vector<LOp> ops2;
                     std::string e2;
                     if (build_schedule(ops2, c2, o2, s2, e2, &sub) != SV_OK) continue;
-                    if (s2.passes.size() < best_passes) {
+                    // ties on the pass count: the modelled time sum_p max(cost_p, H) (H ~ 87 op-cost
+                    // units per HBM pass) when SV_ROLLOUT_BALANCE, else the 1-step score
+                    double model = 0;
+                    if (tie_model)
+                        for (const PassPlan& pp2 : s2.passes) {
+                            double c = 0;
+                            if (pp2.sym)
+                                for (const StageSym& st : pp2.sym->stages)
+                                    for (const LOp& op : st.ops) c += op_cost(op);
+                            model += std::max(c, 87.0);
+                        }
+                    if (s2.passes.size() < best_passes ||
+                        (tie_model && s2.passes.size() == best_passes && model < best_model - 1e-9)) {
                         best_passes = s2.passes.size();
+                        best_model = model;
                         bestmask = cands[k].second;
                     }
                 }
