@@ -39,7 +39,7 @@ METRIC = "gates/s and circuit wall time at 30q; achieved HBM GB/s vs peak at 1/2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--workload", default="supremacy", choices=["supremacy", "multiplier"])
@@ -97,6 +97,16 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_running(self, timeout_s: float = 5.0):
+        """Block until nvidia-smi delivers its first sample (it takes ~0.1-1 s to start), so the
+        samples of a short timed region are not lost to its start-up."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout_s:
+            time.sleep(0.02)
+
+    def mark(self):
+        self.first = len(self.lines)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -108,7 +118,9 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        first = getattr(self, "first", 0)
+        window = self.lines[first:] or self.lines[-1:]  # samples taken during the timed region
+        for ln in window:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 8:
                 continue
@@ -362,8 +374,10 @@ def run_ours(args):
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clk = ClockSampler(local)
     clk.start()
+    clk.wait_running()
     barrier()
     torch.cuda.synchronize()
+    clk.mark()
     t_wall = time.perf_counter()
     for i in range(args.steps):
         e0, e1, e2 = ev[i]
