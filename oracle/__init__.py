@@ -47,6 +47,8 @@ def lib():
         L.or_norm.restype = ctypes.c_double
         L.or_probabilities.argtypes = [ctypes.c_int, dp, ip, ctypes.c_int, dp]
         L.or_classical_map.argtypes = [ctypes.c_char_p, up, up, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int]
+        L.or_classical_map_range.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64, up,
+                                             ctypes.c_char_p, ctypes.c_int]
         L.or_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -136,6 +138,19 @@ def classical_map(text: str, inputs: np.ndarray) -> np.ndarray:
     up = ctypes.POINTER(ctypes.c_uint64)
     if lib().or_classical_map(text.encode(), inp.ctypes.data_as(up), out.ctypes.data_as(up),
                               inp.size, err, 256):
+        raise OracleError(err.value.decode())
+    return out
+
+
+def classical_map_range(text: str, first: int, count: int, out: np.ndarray = None) -> np.ndarray:
+    """f(i) for i in [first, first+count) (bit-sliced, X/SWAP-type gates with controls; first and
+    count multiples of 64).  SURVEY 8(c) comparison step 5."""
+    if out is None:
+        out = np.empty(count, dtype=np.uint64)
+    assert out.dtype == np.uint64 and out.size >= count and out.flags.c_contiguous
+    err = ctypes.create_string_buffer(256)
+    if lib().or_classical_map_range(text.encode(), int(first), int(count),
+                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), err, 256):
         raise OracleError(err.value.decode())
     return out
 

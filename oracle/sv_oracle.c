@@ -429,6 +429,86 @@ int or_classical_map(const char* text, const uint64_t* in, uint64_t* out, uint64
     return 0;
 }
 
+/* Classical reversible map over a whole index range, bit-sliced (SURVEY 8(c) comparison
+ * step 5: "64 indices per uint64 word per gate (Toffoli = AND + XOR on bit planes)").  For
+ * 64 consecutive inputs x = first + 64 w + j, plane[b] holds bit b of the 64 inputs (bit j
+ * of the plane = input j).  Each gate acts on the planes as its classical definition: a
+ * controlled X flips its target where every control is 1 (plane[t] ^= AND of the control
+ * planes); a controlled SWAP exchanges its two targets where every control is 1 and they
+ * differ.  out[64 w + j] = f(first + 64 w + j).  Only X-type and SWAP-type gates (with any
+ * controls) are accepted; first and count must be multiples of 64.  Pinned against the
+ * per-index or_classical_map and the multiplier's a*b (tests/test_oracle.py). */
+int or_classical_map_range(const char* text, uint64_t first, uint64_t count, uint64_t* out, char* err, int errlen) {
+    if ((first | count) & 63) {
+        set_err(err, errlen, "line %d: first and count must be multiples of 64%s", 0, "");
+        return -1;
+    }
+    ocircuit c;
+    if (parse_circuit(text, &c, err, errlen)) return -1;
+    if (c.n > 63) {
+        set_err(err, errlen, "line %d: at most 63 qubits%s", 0, "");
+        free_circuit(&c);
+        return -1;
+    }
+    /* kind[i]: 1 = X on q[nc], 2 = SWAP of q[nc], q[nc+1] */
+    int* kind = (int*)calloc((size_t)c.ngates + 1, sizeof(int));
+    for (int i = 0; i < c.ngates; ++i) {
+        const ogate* g = &c.g[i];
+        const cplx* U = g->U;
+        int isx = g->k == 1;
+        if (isx) {
+            static const double X[8] = {0, 0, 1, 0, 1, 0, 0, 0};
+            for (int e = 0; e < 4; ++e) isx &= U[e].re == X[2 * e] && U[e].im == X[2 * e + 1];
+        }
+        int issw = g->k == 2;
+        if (issw)
+            for (int r = 0; r < 4; ++r)
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int sw = ((cc & 1) << 1) | (cc >> 1);
+                    const double want = (r == sw) ? 1.0 : 0.0;
+                    issw &= U[r * 4 + cc].re == want && U[r * 4 + cc].im == 0.0;
+                }
+        kind[i] = isx ? 1 : issw ? 2 : 0;
+        if (!kind[i]) {
+            set_err(err, errlen, "line %d: not an X- or SWAP-type gate%s", g->line, "");
+            free(kind);
+            free_circuit(&c);
+            return -1;
+        }
+    }
+    static const uint64_t low[6] = {0xAAAAAAAAAAAAAAAAull, 0xCCCCCCCCCCCCCCCCull, 0xF0F0F0F0F0F0F0F0ull,
+                                    0xFF00FF00FF00FF00ull, 0xFFFF0000FFFF0000ull, 0xFFFFFFFF00000000ull};
+    const int n = c.n;
+    const int64_t words = (int64_t)(count / 64);
+#pragma omp parallel for schedule(static)
+    for (int64_t w = 0; w < words; ++w) {
+        const uint64_t base = first + 64 * (uint64_t)w;
+        uint64_t plane[64];
+        for (int b = 0; b < n; ++b) plane[b] = b < 6 ? low[b] : (((base >> b) & 1) ? ~0ull : 0ull);
+        for (int i = 0; i < c.ngates; ++i) {
+            const ogate* g = &c.g[i];
+            uint64_t on = ~0ull;
+            for (int j = 0; j < g->nc; ++j) on &= plane[g->q[j]];
+            if (kind[i] == 1) {
+                plane[g->q[g->nc]] ^= on;
+            } else {
+                const int a = g->q[g->nc], b = g->q[g->nc + 1];
+                const uint64_t d = on & (plane[a] ^ plane[b]);
+                plane[a] ^= d;
+                plane[b] ^= d;
+            }
+        }
+        for (int j = 0; j < 64; ++j) {
+            uint64_t x = 0;
+            for (int b = 0; b < n; ++b) x |= ((plane[b] >> j) & 1ull) << b;
+            out[64 * w + j] = x;
+        }
+    }
+    free(kind);
+    free_circuit(&c);
+    return 0;
+}
+
 int or_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -243,6 +243,79 @@ def test_classical_map_agrees_with_amplitudes():
         oracle.classical_map("qubits: 2\nH 0\n", np.arange(4, dtype=np.uint64))
 
 
+def _py_reversible(gates, x):
+    """Brute-force classical evaluation, one bit at a time (independent of the oracle):
+    ("x", controls, t) flips bit t when every control bit is 1; ("swap", controls, a, b)
+    exchanges bits a and b when every control bit is 1."""
+    for g in gates:
+        if not all((x >> c) & 1 for c in g[1]):
+            continue
+        if g[0] == "x":
+            x ^= 1 << g[2]
+        else:
+            a, b = g[2], g[3]
+            if ((x >> a) ^ (x >> b)) & 1:
+                x ^= (1 << a) | (1 << b)
+    return x
+
+
+def _reversible_text(n, gates):
+    sw = "1,0,0,0,0,0,0,0,0,0,0,0,1,0,0,0,0,0,1,0,0,0,0,0,0,0,0,0,0,0,1,0"  # SWAP, interleaved re,im
+    lines = [f"qubits: {n}"]
+    for g in gates:
+        if g[0] == "x":
+            name = {0: "X", 1: "CNOT", 2: "Toffoli"}.get(len(g[1]))
+            if name:
+                lines.append(f"{name} " + ",".join(str(q) for q in (*g[1], g[2])))
+            else:
+                lines.append(f"CU {','.join(map(str, g[1]))}|{g[2]} : 0,0,1,0,1,0,0,0")
+        elif not g[1]:
+            lines.append(f"SWAP {g[2]},{g[3]}")
+        else:
+            lines.append(f"CU {','.join(map(str, g[1]))}|{g[2]},{g[3]} : {sw}")
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_classical_map_range_brute_force(seed):
+    """SURVEY 8(c) step 5's bit-sliced evaluator (or_classical_map_range) against a bit-by-bit
+    Python evaluation over every input of random X / CNOT / Toffoli / multi-controlled X /
+    SWAP / Fredkin circuits (n = 9), and against the per-index or_classical_map."""
+    rng = np.random.default_rng(100 + seed)
+    n = 9
+    gates = []
+    for _ in range(60):
+        kind = rng.integers(0, 2)
+        nctl = int(rng.integers(0, 4))
+        qs = [int(q) for q in rng.permutation(n)[: nctl + 2]]
+        gates.append(("x", qs[:nctl], qs[nctl]) if kind == 0 else ("swap", qs[:nctl], qs[nctl], qs[nctl + 1]))
+    text = _reversible_text(n, gates)
+    got = oracle.classical_map_range(text, 0, 1 << n)
+    expect = np.array([_py_reversible(gates, x) for x in range(1 << n)], dtype=np.uint64)
+    assert np.array_equal(got, expect)
+    assert np.array_equal(got, oracle.classical_map(text, np.arange(1 << n, dtype=np.uint64)))
+    # a sub-range at an offset gives the same values
+    assert np.array_equal(oracle.classical_map_range(text, 128, 192), expect[128:320])
+
+
+def test_classical_map_range_multiplier_products():
+    """The 31 q 8x7 multiplier over a 2^16 range of inputs with an empty product register:
+    (a, b, 0, 0) -> (a, b, a*b, 0) (closed form), and an arbitrary range equals the per-index map."""
+    c = W.multiplier(8, 7)
+    text = W.to_text(c)
+    got = oracle.classical_map_range(text, 0, 1 << 15)
+    x = np.arange(1 << 15, dtype=np.uint64)
+    a, b = x & 255, x >> 8
+    assert np.array_equal(got, a | (b << 8) | ((a * b) << 15))
+    first = (123457 << 6) * 977 & ((1 << 31) - 1) & ~63
+    got = oracle.classical_map_range(text, first, 4096)
+    assert np.array_equal(got, oracle.classical_map(text, np.arange(first, first + 4096, dtype=np.uint64)))
+    with pytest.raises(oracle.OracleError):
+        oracle.classical_map_range("qubits: 7\nH 0\n", 0, 128)
+    with pytest.raises(oracle.OracleError):
+        oracle.classical_map_range(text, 3, 64)
+
+
 # ------------------------------------------------------------------ determinism, errors
 def test_thread_count_bit_identical():
     """bit-identical for any worker count."""
