@@ -7,14 +7,17 @@ Metric (BASELINE.json): "gates/s and circuit wall time at 30q; achieved HBM GB/s
 is compiled once, outside the timed region, reading R13 T_run).
 
   N = 1 : 30-qubit supremacy-style circuit, 6x5 grid, 20 cycles, 507 gates (BASELINE config 3),
-          complex64 by default (--dtype c128 for the other half of config 3).
-  N > 1 : weak scaling, 2^30 amplitudes per GPU: a (30 + log2 N)-qubit supremacy circuit on a
-          7x5 grid (first n sites) sharded by its top log2 N qubits, global<->local swaps over
-          NCCL.  value = N * gates / step time ("shard-gates/s": every rank applies every gate
-          to its 2^30-amplitude shard).
+          complex64 (--dtype c128 for the other half).  The same JSON line carries, under
+          "also", config 3's other dtype and the config-4 31-qubit multiplier, each timed the
+          same way, and "e2e_cold" (parse + plan + NVRTC + run in a fresh process).
+  N > 1 : BASELINE config 5 (--workload supremacy36, the default): the 36-qubit 6x6 circuit at
+          N = 4 / 8 (35-qubit 7x5 at N = 2, reading R14), sharded by its top log2 N qubits,
+          global<->local swaps through peer memory over NVLink (NCCL fallback).  value = gates /
+          circuit wall time of the whole job (strong: the circuit is fixed).  --workload
+          strong33 (33 q at every N, also N = 1) and weak (2^30 amplitudes per GPU) exist too.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype c64|c128]
-                       [--workload supremacy|multiplier] [--impl ours|reference]
+                       [--workload supremacy|multiplier|supremacy36|strong33|weak] [--impl ours|reference]
 Under torchrun (N > 1) every rank runs; rank 0 prints ONE JSON line.
 """
 
@@ -42,11 +45,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
-    ap.add_argument("--workload", default="supremacy", choices=["supremacy", "multiplier"])
+    ap.add_argument("--workload", default="supremacy",
+                    choices=["supremacy", "multiplier", "supremacy36", "strong33", "weak"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--qubits", type=int, default=30, help="qubits per GPU (default 30)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-also", action="store_true", help="skip the c128 / multiplier sub-lines")
+    ap.add_argument("--no-e2e-cold", action="store_true")
+    ap.add_argument("--e2e-cold-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -54,19 +61,35 @@ def parse():
 def make_workload(args, world: int):
     import workloads as W
     g = world.bit_length() - 1
-    n = args.qubits + g
     if args.workload == "supremacy":
-        if n == 30:
-            c = W.supremacy(6, 5, 20, seed=0)
-            name = "supremacy 6x5 grid, 20 cycles, seed 0"
+        if args.qubits != 30 or world != 1:
+            raise SystemExit("--workload supremacy is BASELINE config 3 (30 qubits, 1 GPU); "
+                             "use supremacy36 / strong33 / weak for N > 1")
+        c = W.supremacy(6, 5, 20, seed=0)
+        name = "supremacy 6x5 grid, 20 cycles, seed 0"
+    elif args.workload == "supremacy36":
+        # BASELINE config 5: 36 q (6x6 grid) at P = 4 / 8; 35 q (7x5) at P = 2 (reading R14:
+        # 36 q c64 needs 256 GiB per GPU at P = 2)
+        if world >= 4:
+            c = W.supremacy(6, 6, 20, seed=0)
+            name = "supremacy 6x6 grid (36 q), 20 cycles, seed 0"
         else:
-            rows = (n + 4) // 5
-            c = W.supremacy(rows, 5, 20, seed=0, n=n)
-            name = f"supremacy {rows}x5 grid (first {n} sites), 20 cycles, seed 0"
+            c = W.supremacy(7, 5, 20, seed=0)
+            name = "supremacy 7x5 grid (35 q; 36 q does not fit 2 GPUs, R14), 20 cycles, seed 0"
+    elif args.workload == "strong33":
+        # strong scaling: the same 33-qubit circuit at every N (SURVEY 8(d) c5 series)
+        c = W.supremacy(7, 5, 20, seed=0, n=33)
+        name = "supremacy 7x5 grid (first 33 sites), 20 cycles, seed 0"
+    elif args.workload == "weak":
+        # weak scaling: 2^qubits amplitudes per GPU, (qubits + log2 N)-qubit circuit
+        n = args.qubits + g
+        rows = (n + 4) // 5
+        c = W.supremacy(rows, 5, 20, seed=0, n=n)
+        name = f"supremacy {rows}x5 grid (first {n} sites), 20 cycles, seed 0"
     else:
-        # 31q multiplier (BASELINE config 4): rectangular 8x7 (reading R7), basis-free uniform input
-        if n != 31:
-            raise SystemExit("--workload multiplier is defined for 31 qubits (use --qubits 31)")
+        # 31q multiplier (BASELINE config 4): rectangular 8x7 (reading R7), uniform input
+        if args.qubits != 31 or world != 1:
+            raise SystemExit("--workload multiplier is config 4 (use --qubits 31, one GPU)")
         c = W.multiplier(8, 7)
         name = "multiplier 8x7 (shift-and-add Cuccaro), 455 gates"
     return c, W.to_text(c), name
@@ -278,7 +301,10 @@ def run_reference(args):
         return
     import numpy as np
     import oracle
-    c, text, name = make_workload(args, 1)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and args.workload == "supremacy" and args.qubits == 30:
+        args.workload = "supremacy36"  # the same config as our arm at N > 1 (config 5)
+    c, text, name = make_workload(args, world)
     n = c.n
     avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
     n_eff = n
@@ -318,7 +344,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": (secs / max(1, args.steps)) * 1e3 if secs else None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": name, "n_qubits": n, "gates": G},
             "cpu_baseline": {"value": value, "unit": "gates/s", "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": sample},
@@ -327,6 +353,196 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def host_info():
+    """CPU model, sockets, logical cores and host RAM of the box (reported with the
+    oracle baseline)."""
+    model, sockets = None, set()
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name") and model is None:
+                model = ln.split(":", 1)[1].strip()
+            elif ln.startswith("physical id"):
+                sockets.add(ln.split(":", 1)[1].strip())
+    except Exception:
+        pass
+    try:
+        ram = int([l for l in open("/proc/meminfo") if l.startswith("MemTotal")][0].split()[1]) * 1024
+    except Exception:
+        ram = None
+    return {"cpu_model": model, "sockets": len(sockets) or None, "logical_cpus": os.cpu_count(),
+            "host_ram_gib": round(ram / 2 ** 30, 1) if ram else None}
+
+
+def time_case(P, torch, sv, c, text, dtype, workload, steps, warmup, world, local, barrier, per_pass=True):
+    """Time K steps of one workload on an existing state (barrier + synchronize on both sides,
+    CUDA events on the state's stream, max over ranks) and compute its roofline.  One step =
+    init (deferred into the first pass on one GPU) + every pass of the compiled plan."""
+    from paper_2106_13995_b200.dist import max_over_ranks
+    n = c.n
+    G = len(c.gates)
+    stream = torch.cuda.ExternalStream(sv.stream_ptr())
+    plan = P.Plan(text, dtype)
+    # timing input: |0...0> for supremacy (its own H layer makes the superposition, reading
+    # R5); the uniform superposition for the multiplier (P:69, SURVEY 8(d) c4).  On one GPU
+    # both inits are deferred: the plan's first tile pass synthesises its input tile instead
+    # of reading it (a fill / memset kernel when the state is sharded)
+    init = sv.init_uniform if workload == "multiplier" else sv.init_zero
+    st = None
+    for _ in range(warmup):
+        init()
+        st = sv.apply_plan(plan)
+    sv.sync()
+    info = plan.info()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    clk = ClockSampler(local)
+    clk.start()
+    clk.wait_running()
+    barrier()
+    torch.cuda.synchronize()
+    clk.mark()
+    t_wall = time.perf_counter()
+    for i in range(steps):
+        e0, e1, e2 = ev[i]
+        e0.record(stream)
+        init()
+        e1.record(stream)
+        st = sv.apply_plan(plan)
+        e2.record(stream)
+    sv.sync()
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - t_wall
+    clocks = clk.stop()
+    total_ms = sum(e0.elapsed_time(e2) for e0, _, e2 in ev)
+    tpass_ms = sum(e1.elapsed_time(e2) for _, e1, e2 in ev)
+    if world > 1:
+        total_ms, tpass_ms = max_over_ranks([total_ms, tpass_ms])
+    ms_per_step = total_ms / steps
+    amp = 16 if dtype == "c128" else 8
+    local_amps = 1 << (n - (world.bit_length() - 1))
+    launches = max(1, st["launches"])
+    # algorithmic bytes of the passes as the library counts them (2 x state per pass; a first
+    # pass that synthesises a deferred basis state writes only)
+    bytes_per_launch = st["hbm_bytes"] / launches
+    avg_launch_ms = tpass_ms / (steps * launches)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    # Roofline of the pass kernel family: the HBM floor (2 x state bytes per launch) and the
+    # FP-pipe floor (algorithmic lane-ops); "bound" is the larger floor.
+    hbm_roof = {"achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": achieved / peak, "bytes_per_launch": bytes_per_launch}
+    kernel = ("generated relabel + permutation (gather) passes" if workload == "multiplier"
+              else "tile_pass_kernel (generated, one per pass)")
+    traffic_key = workload if workload in ("supremacy", "multiplier") else "supremacy"
+    roofline = {"bound": "hbm", "kernel": kernel, **hbm_roof,
+                "traffic": profiled_traffic(traffic_key, dtype), "avg_launch_ms": avg_launch_ms}
+    opa = alg_ops_per_amp(c, launches)
+    if opa:
+        ops_per_launch = opa * local_amps / launches
+        a_alu = ops_per_launch / (avg_launch_ms / 1e3) / 1e12
+        p_alu = alu_peak(dtype)
+        alu_roof = {"achieved": a_alu, "peak": p_alu, "unit": "TFLOP/s", "frac": a_alu / p_alu,
+                    "peak_source": "derived: 148 SMs x %d lanes x max SM clock (DESIGN.md 6)"
+                                   % (64 if dtype == "c128" else 128),
+                    "flops_per_amp": opa, "flops_per_launch": ops_per_launch}
+        t_hbm = bytes_per_launch / (peak * 1e9)
+        t_alu = ops_per_launch / (p_alu * 1e12)
+        if t_alu > t_hbm:
+            roofline = {"bound": "alu", "kernel": kernel, **alu_roof,
+                        "traffic": profiled_traffic(traffic_key, dtype), "avg_launch_ms": avg_launch_ms}
+        roofline["hbm"] = hbm_roof
+        roofline["alu"] = alu_roof
+        roofline["floor_frac"] = max(t_hbm, t_alu) * 1e3 / avg_launch_ms
+    # Per-pass breakdown (single GPU, outside the timed region): the same plan compiled with
+    # per-pass CUDA events, three back-to-back runs; each pass's algorithmic HBM bytes (2 x
+    # state, 1 x for a first pass that synthesises its input) over its own duration.
+    if world == 1 and per_pass:
+        try:
+            pplan = P.Plan(text, dtype, profile=True)
+            for _ in range(3):
+                init()
+                pst = sv.apply_plan(pplan)
+            pt = pplan.pass_times()
+            state_b = local_amps * amp
+            synth = pst["hbm_bytes"] < 2 * state_b * pst["launches"]  # first launch synthesises its input
+            per = []
+            for i, ms in enumerate(pt):
+                if i + 1 < len(pt) and pt[i + 1] < 0.005:
+                    kind = "pair"  # this pass and the next one in one kernel (through L2)
+                elif ms < 0.005:
+                    per.append({"ms": 0.0, "kind": "paired (ran in the previous launch)"})
+                    continue
+                else:
+                    kind = "pass"
+                b = state_b * (1 if i == 0 and synth else 2)
+                per.append({"ms": round(ms, 4), "kind": kind, "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 3)})
+            roofline["per_pass"] = per
+            pplan.close()
+        except Exception as e:  # report, never hide
+            roofline["per_pass"] = f"unavailable: {e}"
+    plan.close()
+    return {"G": G, "n": n, "ms_per_step": ms_per_step, "value": G / (ms_per_step / 1e3), "st": st,
+            "info": info, "launches": launches, "achieved": achieved, "roofline": roofline, "clocks": clocks,
+            "wall": wall, "local_amps": local_amps, "amp": amp, "init": init}
+
+
+def e2e_cold_child(args):
+    """--e2e-cold-child: in a fresh process (empty plan and NVRTC caches), time the first
+    sv_apply_circuit of the workload from IR text (parse + plan + NVRTC + init + passes) plus
+    the marginal read-back, then the parse + plan part alone (a second Plan compile of the same
+    text; it does not touch the kernel cache) and a warm run.  Prints one JSON object."""
+    import torch
+    import paper_2106_13995_b200 as P
+    torch.cuda.set_device(0)
+    c, text, name = make_workload(args, 1)
+    n = c.n
+    sv = P.StateVector(n, args.dtype)
+    q = list(range(min(20, n)))
+    init = sv.init_uniform if args.workload == "multiplier" else sv.init_zero
+    sv.sync()
+    t0 = time.perf_counter()
+    init()
+    sv.apply_circuit(text)
+    sv.probabilities(q)
+    cold = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan = P.Plan(text, args.dtype)
+    plan_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    init()
+    sv.apply_circuit(text)
+    sv.probabilities(q)
+    warm = time.perf_counter() - t0
+    print(json.dumps({"cold_ms": cold * 1e3, "parse_plan_ms": plan_s * 1e3, "warm_ms": warm * 1e3,
+                      "nvrtc_and_first_launch_ms": (cold - plan_s - warm) * 1e3}), flush=True)
+    plan.close()
+    sv.close()
+
+
+def e2e_cold(args, G):
+    cmd = [sys.executable, os.path.abspath(__file__), "--e2e-cold-child", "--dtype", args.dtype,
+           "--workload", args.workload, "--qubits", str(args.qubits)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        d["value"] = G / (d["cold_ms"] / 1e3)
+        d["unit"] = "gates/s"
+        d["includes"] = ("fresh process: IR text -> parse + plan + NVRTC code generation + init + passes + "
+                         "20-qubit marginal D2H, first call (SURVEY R13 T_e2e)")
+        return d
+    except Exception as e:  # report, never hide
+        return {"value": None, "unit": "gates/s", "error": str(e)[:300]}
+
+
+def sub_line(res, dtype, name):
+    return {"workload": name, "state_dtype": "complex128" if dtype == "c128" else "complex64",
+            "dtype": "f64" if dtype == "c128" else "f32", "n_qubits": res["n"], "gates": res["G"],
+            "value": res["value"], "unit": "gates/s", "ms_per_step": res["ms_per_step"],
+            "passes_per_step": res["st"]["passes"], "roofline": res["roofline"], "clocks": res["clocks"],
+            "gpu_launches": res["launches"]}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -342,6 +558,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 and args.workload == "supremacy" and args.qubits == 30:
+        args.workload = "supremacy36"  # BASELINE config 5 is the N > 1 workload
     c, text, name = make_workload(args, world)
     n = c.n
     G = len(c.gates)
@@ -349,109 +567,16 @@ def run_ours(args):
         sv = P.StateVector.sharded(n, args.dtype)
     else:
         sv = P.StateVector(n, args.dtype)
-    stream = torch.cuda.ExternalStream(sv.stream_ptr())
-    plan = P.Plan(text, args.dtype)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # warm-up (also compiles + caches the schedule)
-    st = None
-    # timing input: |0...0> for supremacy (its own H layer makes the superposition, reading
-    # R5); the uniform superposition for the multiplier.  Both inits
-    # are deferred on one GPU: the plan's first tile pass synthesises its input tile instead
-    # of reading it (a fill / memset kernel when the state is sharded)
-    init = sv.init_uniform if args.workload == "multiplier" else sv.init_zero
-    for _ in range(args.warmup):
-        init()
-        st = sv.apply_plan(plan)
-    sv.sync()
-    passes = st["passes"] if st else 0
-    info = plan.info()
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clk = ClockSampler(local)
-    clk.start()
-    clk.wait_running()
-    barrier()
-    torch.cuda.synchronize()
-    clk.mark()
-    t_wall = time.perf_counter()
-    for i in range(args.steps):
-        e0, e1, e2 = ev[i]
-        e0.record(stream)
-        init()
-        e1.record(stream)
-        st = sv.apply_plan(plan)
-        e2.record(stream)
-    sv.sync()
-    torch.cuda.synchronize()
-    barrier()
-    wall = time.perf_counter() - t_wall
-    clocks = clk.stop()
-    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
-    pass_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev]
-    total_ms = sum(step_ms)
-    tpass_ms = sum(pass_ms)
-    if world > 1:
-        total_ms, tpass_ms = max_over_ranks([total_ms, tpass_ms])
-    ms_per_step = total_ms / args.steps
-    value = world * G / (ms_per_step / 1e3)
-    amp = 16 if args.dtype == "c128" else 8
-    local_amps = 1 << (n - (world.bit_length() - 1))
-    launches = max(1, st["launches"])
-    # algorithmic bytes of the passes as the library counts them (2 x state per pass; a first
-    # pass that synthesises a deferred basis state writes only)
-    bytes_per_launch = st["hbm_bytes"] / launches
-    avg_launch_ms = tpass_ms / (args.steps * launches)
-    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
-    peak, peak_src = measured_peak_hbm()
-
-    # Roofline of the tile-pass kernel family: the HBM floor (2 x state bytes per launch) and
-    # the FP-pipe floor (algorithmic lane-ops); "bound" is the larger floor.
-    hbm_roof = {"achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": achieved / peak, "bytes_per_launch": bytes_per_launch}
-    opa = alg_ops_per_amp(c, launches)
-    roofline = {"bound": "hbm", "kernel": "tile_pass_kernel (generated, one per pass)", **hbm_roof,
-                "traffic": profiled_traffic(args.workload, args.dtype), "avg_launch_ms": avg_launch_ms}
-    if opa:
-        ops_per_launch = opa * local_amps / launches
-        a_alu = ops_per_launch / (avg_launch_ms / 1e3) / 1e12
-        p_alu = alu_peak(args.dtype)
-        alu_roof = {"achieved": a_alu, "peak": p_alu, "unit": "TFLOP/s", "frac": a_alu / p_alu,
-                    "peak_source": "derived: 148 SMs x %d lanes x max SM clock (DESIGN.md 7)"
-                                   % (64 if args.dtype == "c128" else 128),
-                    "flops_per_amp": opa, "flops_per_launch": ops_per_launch}
-        t_hbm = bytes_per_launch / (peak * 1e9)
-        t_alu = ops_per_launch / (p_alu * 1e12)
-        if t_alu > t_hbm:
-            roofline = {"bound": "alu", "kernel": roofline["kernel"], **alu_roof,
-                        "traffic": profiled_traffic(args.workload, args.dtype), "avg_launch_ms": avg_launch_ms}
-        roofline["hbm"] = hbm_roof
-        roofline["alu"] = alu_roof
-        roofline["floor_frac"] = max(t_hbm, t_alu) * 1e3 / avg_launch_ms
-
-    # Per-pass breakdown (single GPU, outside the timed region): the same plan compiled with
-    # per-pass CUDA events, three back-to-back runs; each pass's algorithmic HBM bytes (2 x
-    # state, 1 x for a first pass that synthesises its input) over its own duration.
-    if world == 1:
-        try:
-            pplan = P.Plan(text, args.dtype, profile=True)
-            for _ in range(3):
-                init()
-                pst = sv.apply_plan(pplan)
-            pt = pplan.pass_times()
-            state_b = local_amps * amp
-            per = []
-            for i, ms in enumerate(pt):
-                b = state_b * (1 if i == 0 and pst["hbm_bytes"] < 2 * state_b * len(pt) else 2)
-                per.append({"ms": round(ms, 4), "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 3)})
-            roofline["per_pass"] = per
-            pplan.close()
-        except Exception as e:  # report, never hide
-            roofline["per_pass"] = f"unavailable: {e}"
+    res = time_case(P, torch, sv, c, text, args.dtype, args.workload, args.steps, args.warmup, world, local,
+                    barrier)
+    st, info, init = res["st"], res["info"], res["init"]
+    ms_per_step = res["ms_per_step"]
+    launches = res["launches"]
 
     # e2e: same metric through the public API with host buffers: IR text in, parse + plan +
     # init + apply, marginal probabilities of 20 qubits (8 MiB fp64) back to the host.
@@ -471,25 +596,49 @@ def run_ours(args):
     if world > 1:
         (e2e_s,) = max_over_ranks([e2e_s])
     assert abs(probs.sum() - 1.0) < 1e-3
+    sv.close()
+
+    # The rest of configs 3 and 4 on one GPU, each timed the same way:
+    # config 3's complex128 half and the config-4 31-qubit multiplier (uniform input).
+    also = {}
+    if world == 1 and not args.no_also and args.workload == "supremacy" and args.qubits == 30:
+        import workloads as W
+        for key, dtype, wl, circ, nm in (
+                ("supremacy30_c128" if args.dtype == "c64" else "supremacy30_c64",
+                 "c128" if args.dtype == "c64" else "c64", "supremacy", W.supremacy(6, 5, 20, seed=0), name),
+                ("multiplier31_c64", "c64", "multiplier", W.multiplier(8, 7),
+                 "multiplier 8x7 (shift-and-add Cuccaro), 455 gates, uniform input")):
+            try:
+                with P.StateVector(circ.n, dtype) as sv2:
+                    r2 = time_case(P, torch, sv2, circ, W.to_text(circ), dtype, wl, args.steps, args.warmup, 1,
+                                   local, barrier)
+                also[key] = sub_line(r2, dtype, nm)
+            except Exception as e:  # report, never hide
+                also[key] = {"error": str(e)[:300]}
+
+    cold = e2e_cold(args, G) if (world == 1 and rank == 0 and not args.no_e2e_cold) else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline(text, n, args.cpu_seconds)
+            cpu.update(host_info())
         except Exception as e:  # report, never hide
             cpu = {"value": None, "unit": "gates/s", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
 
     if rank == 0:
+        g = world.bit_length() - 1
+        scaling = "weak" if args.workload == "weak" else "strong"
         line = {
             "metric": METRIC,
-            "value": value,
+            "value": res["value"],
             "unit": "gates/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": scaling,
             "vs_baseline": None,
             "dtype": "f64" if args.dtype == "c128" else "f32",  # arithmetic type (complex64 state: FP32)
             "data": "synthetic",
@@ -497,33 +646,34 @@ def run_ours(args):
                 "workload": name,
                 "state_dtype": "complex128" if args.dtype == "c128" else "complex64",
                 "n_qubits": n,
-                "n_qubits_per_gpu": n - (world.bit_length() - 1),
+                "n_qubits_per_gpu": n - g,
                 "gates": G,
-                "passes_per_step": passes,
+                "passes_per_step": st["passes"],
                 "stages_per_step": info.get("stages"),
                 "swaps_per_step": st.get("swaps", 0),
-                "state_bytes_per_gpu": local_amps * amp,
+                "state_bytes_per_gpu": res["local_amps"] * res["amp"],
                 "timed": ("init uniform superposition" if args.workload == "multiplier" else "init |0...0>")
-                         + (" (fill kernel) + all passes" if world > 1 else
+                         + (" (fill kernel) + all passes and exchange steps" if world > 1 else
                             " (deferred, synthesised by the first pass) + all passes")
                          + " (plan compiled once, outside the timed region)",
                 "l2": "state (>= 8 GiB per GPU) is larger than L2 (126 MB): no flush needed",
-                "parallelism": f"sharded by top {world.bit_length() - 1} qubits" if world > 1 else "single GPU",
+                "parallelism": f"sharded by top {g} qubits over {world} GPUs" if world > 1 else "single GPU",
+                "value_is": "circuit gates (IR gates, R12) / circuit wall time; whole job",
             },
             "circuit_wall_ms": ms_per_step,
-            "hbm_gbs": achieved,
-            "roofline": roofline,
+            "hbm_gbs": res["achieved"],
+            "roofline": res["roofline"],
             "cpu_baseline": cpu,
-            "e2e": {"value": world * G / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": len(text.encode()),
+            "e2e": {"value": G / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": len(text.encode()),
                     "d2h_bytes_per_step": 8 * len(probs),
                     "includes": "IR text through sv_apply_circuit (plan cache warm) + init + passes + 20-qubit marginal D2H"},
+            "e2e_cold": cold,
+            "also": also or None,
             "gpu_launches": int(args.steps * launches),
-            "clocks": clocks,
-            "wall_s_timed_region": wall,
+            "clocks": res["clocks"],
+            "wall_s_timed_region": res["wall"],
         }
         print(json.dumps(line), flush=True)
-    sv.close()
-    plan.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -532,7 +682,9 @@ def main():
     args = parse()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.e2e_cold_child:
+        e2e_cold_child(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

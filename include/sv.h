@@ -72,7 +72,8 @@ typedef enum {
 typedef struct {
     int fuse;            /* 1 (default) = fuse gates into multi-stage tile passes */
     int tile_qubits;     /* m, qubits per tile pass; 0 = auto */
-    int max_fused_k;     /* reserved: largest pre-multiplied dense block (0 = none) */
+    int max_fused_k;     /* unused (ABI slot): the planner fuses by stages and passes, never by
+                            pre-multiplying blocks; must be 0 */
     int force_kernel;    /* sv_kernel */
     int check_unitary;   /* 1 = reject matrices with |U^dagger U - I| > 1e-9 */
     int use_graph;       /* 1 = record the plan's launches into a CUDA graph on first use */
@@ -104,8 +105,12 @@ uint64_t sv_memory_estimate(int n, sv_dtype dtype);
  * private non-blocking stream.  SV_ERR_RESOURCE if the allocation fails. */
 sv_status sv_create(int n, sv_dtype dtype, void* stream, sv_state* out);
 
-/* Wrap a caller-owned device buffer of 2^n amplitudes (e.g. a torch tensor).  The
- * buffer contents are left as they are; the handle never frees it. */
+/* Wrap a caller-owned device buffer of 2^n amplitudes (e.g. a torch tensor; the
+ * state is the 2^n amplitude vector in index order).  The buffer contents are left as they
+ * are; the handle never frees it.  Every call that changes the state leaves the buffer in
+ * logical index order once its work on the stream completes (a relabelling plan's final
+ * layout is undone inside sv_plan_apply / sv_apply_circuit for borrowed buffers), so the
+ * caller may read the tensor after synchronising the stream (sv_sync or its own sync). */
 sv_status sv_wrap(int n, sv_dtype dtype, void* dev_ptr, void* stream, sv_state* out);
 
 /* NCCL bootstrap for sharded states: rank 0 writes a 128-byte unique id into out_128B;
@@ -117,6 +122,32 @@ sv_status sv_nccl_unique_id(void* out_128B);
  * physical qubits equal r.  State = |0...0>. */
 sv_status sv_create_sharded(int n, sv_dtype dtype, const void* uid_128B, int world, int rank,
                             void* stream, sv_state* out);
+
+/* Host control plane for sharded states (alternative to NCCL's): the library needs only an
+ * all-gather of small host messages and a barrier across the ranks.  Each callback returns
+ * 0 on success and is called collectively (every rank, same order) from the thread making
+ * the sv_* call.  allgather: every rank contributes `bytes` bytes from `in`; `out` receives
+ * world * bytes bytes in rank order.  barrier: returns when every rank has entered it.
+ * With a host control plane the library synchronises the state's stream before each
+ * barrier, and every global<->local exchange goes through peer memory (CUDA IPC mappings of
+ * every rank's buffer pair: remote stores fused into the preceding pass, or a peer-copy
+ * kernel); there is no NCCL communicator.  This is how several ranks can share one GPU. */
+typedef struct {
+    void* user;
+    int (*allgather)(void* user, const void* in, size_t bytes, void* out);
+    int (*barrier)(void* user);
+} sv_control;
+
+/* Collective: a sharded state as sv_create_sharded, with either an NCCL unique id
+ * (uid_128B != NULL, ctl == NULL) or a host control plane (ctl != NULL, uid_128B == NULL).
+ * dev_ptr: NULL = allocate the local shard of 2^(n-g) amplitudes; else a caller-owned
+ * device buffer of that size, borrowed (never freed), which holds the local shard in
+ * logical order whenever a call's work completes.  The peer-memory exchange
+ * allocates a second shard buffer; SV_ERR_RESOURCE if that fails with a host control plane
+ * (there is no NCCL fallback there).  Errors as sv_create_sharded; SV_ERR_ARG if both or
+ * neither of uid_128B and ctl are given. */
+sv_status sv_create_sharded_ex(int n, sv_dtype dtype, const void* uid_128B, const sv_control* ctl, int world,
+                               int rank, void* dev_ptr, void* stream, sv_state* out);
 
 /* Single-process emulation of a `world`-way sharded state on one GPU (tests): the shards
  * are slices of one allocation and the all-to-all is device-to-device copies.  Runs the
@@ -182,11 +213,14 @@ sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* o
                            sv_run_stats* stats);
 
 /* Read amplitudes [first, first+count) of the logical state into host_out (interleaved,
- * state dtype).  Synchronises.  Sharded: each rank receives the part of the range it holds
+ * state dtype).  P:38 (the state is the 2^n amplitude vector), S:112-120 (amplitude
+ * readout).  A relabelled layout (sv_qubit_map not the identity) is first made canonical on
+ * the device.  Synchronises.  SV_ERR_RANGE if the range exceeds 2^n.  Sharded: each rank receives the part of the range it holds
  * (after the qubit map is made canonical) at host_out + (index - first). */
 sv_status sv_amplitudes(sv_state s, uint64_t first, uint64_t count, void* host_out);
 
-/* Marginal probabilities of the qubit subset: host_out[k] = sum over basis states whose
+/* P:38 (|a_i|^2 are the outcome probabilities of the 2^n basis states), S:92-100,
+ * reading R11.  Marginal probabilities of the qubit subset: host_out[k] = sum over basis states whose
  * bit qubits[j] equals bit j of k of |a|^2, accumulated in fp64 in a fixed order
  * (deterministic), 2^nq doubles.  0 <= nq <= min(n, 28).  Sharded: global value on every rank. */
 sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_out);
@@ -194,13 +228,24 @@ sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_o
 /* sqrt(sum |a_i|^2) accumulated in fp64 with a fixed-order tree. */
 sv_status sv_norm(sv_state s, double* out);
 
+/* Wait for every launched call on the handle's stream (calls are asynchronous,
+ * readouts synchronise).  A deferred initialisation (sv_init_*) is written first.  Does NOT
+ * change the layout: an owned state may be left relabelled by its last plan (sv_qubit_map);
+ * use sv_device_ptr or the readouts for index order.  Borrowed buffers are always in index
+ * order (sv_wrap).  Returns SV_ERR_CUDA for an asynchronous fault of an earlier launch. */
 sv_status sv_sync(sv_state s);
 
 /* Introspection for the bindings and the bench. */
 sv_status sv_info(sv_state s, int* n, int* n_local, int* world, int* rank, sv_dtype* dtype);
+/* Device pointer of the (local) state buffer and its amplitude count.  Makes the layout
+ * canonical first (logical index order; on the stream, asynchronous).  The pointer is valid
+ * until the next call that applies gates: a permutation (gather) pass of an owned state
+ * writes the other buffer of a pair and swaps them, so re-query after every apply. */
 sv_status sv_device_ptr(sv_state s, void** dev_ptr, uint64_t* local_amps);
 sv_status sv_stream(sv_state s, void** stream);
-/* Current physical position of every logical qubit (phys[q]); identity unless swaps ran. */
+/* Current physical position of every logical qubit (phys[q]).  Not the identity after a
+ * relabelling single-GPU plan (owned states) or sharded exchange steps; readouts,
+ * sv_device_ptr and sv_set_amplitudes restore the identity. */
 sv_status sv_qubit_map(sv_state s, int* phys_out);
 
 const char* sv_last_error(void);

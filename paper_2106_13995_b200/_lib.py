@@ -28,6 +28,15 @@ class RunOpts(ctypes.Structure):
                 ("profile", ctypes.c_int), ("exchange", ctypes.c_int)]
 
 
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+
+
+class Control(ctypes.Structure):
+    """sv_control: host control plane of a sharded state (all-gather + barrier callbacks)."""
+    _fields_ = [("user", ctypes.c_void_p), ("allgather", ALLGATHER_FN), ("barrier", BARRIER_FN)]
+
+
 class RunStats(ctypes.Structure):
     _fields_ = [("gates", ctypes.c_uint64), ("passes", ctypes.c_uint64), ("stages", ctypes.c_uint64),
                 ("swaps", ctypes.c_uint64), ("launches", ctypes.c_uint64), ("hbm_bytes", ctypes.c_uint64),
@@ -52,6 +61,7 @@ def _load():
         "sv_nccl_unique_id": (i, [vp]),
         "sv_create_sharded": (i, [i, i, vp, i, i, vp, ctypes.POINTER(vp)]),
         "sv_create_virtual_sharded": (i, [i, i, i, vp, ctypes.POINTER(vp)]),
+        "sv_create_sharded_ex": (i, [i, i, vp, ctypes.POINTER(Control), i, i, vp, vp, ctypes.POINTER(vp)]),
         "sv_destroy": (i, [vp]),
         "sv_init_zero": (i, [vp]),
         "sv_init_basis": (i, [vp, u64]),
@@ -87,6 +97,7 @@ def _load():
 
 lib = _load()
 EXPORTED = ["sv_memory_estimate", "sv_create", "sv_wrap", "sv_nccl_unique_id", "sv_create_sharded",
+            "sv_create_sharded_ex",
             "sv_create_virtual_sharded", "sv_destroy", "sv_init_zero", "sv_init_basis", "sv_init_uniform",
             "sv_set_amplitudes", "sv_apply_gate", "sv_plan_compile", "sv_plan_info", "sv_plan_qubit_map", "sv_plan_source",
             "sv_plan_destroy", "sv_plan_pass_times", "sv_plan_shard_info",

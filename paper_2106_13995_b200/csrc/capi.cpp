@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <chrono>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <cmath>
 #include <cstdio>
@@ -116,9 +117,13 @@ void free_state(sv_state_s* s) {
     if (!s) return;
     for (void* q : s->ipc_open) cudaIpcCloseMemHandle(q);
     if (s->xflag) cudaFree(s->xflag);
-    if (s->owned && s->d) cudaFree(s->d);
-    if (s->d2) cudaFree(s->d2);
+    // d and d2 may have been swapped (permutation passes, peer-memory flips): free what is
+    // ours, never the borrowed buffer
+    if (s->d && s->d != s->user_buf) cudaFree(s->d);
+    if (s->d2 && s->d2 != s->user_buf) cudaFree(s->d2);
+    if (s->d_gather) cudaFree(s->d_gather);
     if (s->d_scratch) cudaFree(s->d_scratch);
+    if (s->pair_ctl) cudaFree(s->pair_ctl);
     if (s->xbuf) cudaFree(s->xbuf);
     if (s->comm) comm_destroy(s->comm);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
@@ -147,6 +152,36 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
     for (const PassPlan& pp : sc.passes) {
         ++pi;
         cudaError_t e;
+        if (pp.paired_second) {
+            // ran inside the previous pass's pair kernel
+            if (ev) CK(cudaEventRecord((*ev)[pi], s->stream));
+            if (st) st->passes += 1;
+            continue;
+        }
+        if (pp.kind == PassPlan::TILE && pp.pair_fn) {
+            const size_t need = (size_t)(pp.pair_chunks + 1) * 8;
+            if (s->pair_ctl_bytes < need) {
+                if (s->pair_ctl) cudaFree(s->pair_ctl);
+                s->pair_ctl = nullptr;
+                s->pair_ctl_bytes = 0;
+                CK(cudaMalloc(&s->pair_ctl, need));
+                s->pair_ctl_bytes = need;
+            }
+            const int variant = (pi == 1 && basis >= 0) ? 1 : (pi == 1 && uniform) ? 2 : 0;
+            e = jit_launch_pair(pp, psi, s->pair_ctl, variant, basis >= 0 ? (uint64_t)basis : 0, uniform_amp(s->n),
+                                s->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "pair launch");
+            if (ev) CK(cudaEventRecord((*ev)[pi], s->stream));
+            if (st) {
+                st->passes += 1;
+                st->launches += 1;
+                st->stages += pp.nstages;
+                // one read (none when the input is synthesised) and one write of the state for
+                // both passes: the second pass reads the first's output from L2
+                st->hbm_bytes += (variant ? 1ull : 2ull) * pp.touched_amps * s->amp_bytes();
+            }
+            continue;
+        }
         if (pp.kind == PassPlan::PERM) {
             // out-of-place gather into the scratch state, then swap the buffers (or copy back
             // into a borrowed buffer)
@@ -317,6 +352,7 @@ sv_status sv_wrap(int n, sv_dtype dtype, void* dev_ptr, void* stream, sv_state* 
     sv_status st = new_state(n, n, 1, 0, dtype, stream, &s);
     if (st != SV_OK) return st;
     s->d = dev_ptr;
+    s->user_buf = dev_ptr;
     *out = s;
     return SV_OK;
 }
@@ -359,40 +395,54 @@ sv_status sv_nccl_unique_id(void* out_128B) {
     return SV_OK;
 }
 
-sv_status sv_create_sharded(int n, sv_dtype dtype, const void* uid, int world, int rank, void* stream,
-                            sv_state* out) {
-    if (!out || !uid) return fail(SV_ERR_ARG, "NULL argument");
+sv_status sv_create_sharded_ex(int n, sv_dtype dtype, const void* uid, const sv_control* ctl, int world, int rank,
+                               void* dev_ptr, void* stream, sv_state* out) {
+    if (!out) return fail(SV_ERR_ARG, "NULL out");
+    if ((uid == nullptr) == (ctl == nullptr))
+        return fail(SV_ERR_ARG, "exactly one of uid_128B (NCCL) and ctl (host control plane) must be given");
+    if (ctl && (!ctl->allgather || !ctl->barrier)) return fail(SV_ERR_ARG, "sv_control without callbacks");
     if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
-    if (world < 2 || (world & (world - 1)) || rank < 0 || rank >= world)
-        return fail(SV_ERR_ARG, "world must be a power of two >= 2 and 0 <= rank < world");
+    if (world < 2 || world > 8 || (world & (world - 1)) || rank < 0 || rank >= world)
+        return fail(SV_ERR_ARG, "world must be 2, 4 or 8 and 0 <= rank < world");
     int g = 0;
     while ((1 << g) < world) ++g;
-    if (n - g < 1 || n > 44) return fail(SV_ERR_RANGE, "bad n for this world size");
+    if (n - g < g + 1 || n > 44) return fail(SV_ERR_RANGE, "bad n for this world size (need n - log2(world) > log2(world))");
     sv_state_s* s;
     sv_status st = new_state(n, n - g, world, rank, dtype, stream, &s);
     if (st != SV_OK) return st;
     const size_t bytes = (size_t)s->local_amps() * s->amp_bytes();
-    cudaError_t e = cudaMalloc(&s->d, bytes);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        free_state(s);
-        return fail(SV_ERR_RESOURCE, "cannot allocate the local shard: needs " + std::to_string(bytes) +
-                                         " bytes per GPU (" + bytes_str(n, dtype) + " total)");
+    if (dev_ptr) {
+        s->d = dev_ptr;
+        s->user_buf = dev_ptr;
+    } else {
+        cudaError_t e = cudaMalloc(&s->d, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            free_state(s);
+            return fail(SV_ERR_RESOURCE, "cannot allocate the local shard: needs " + std::to_string(bytes) +
+                                             " bytes per GPU (" + bytes_str(n, dtype) + " total)");
+        }
+        s->owned = true;
     }
-    s->owned = true;
     std::string err;
-    st = comm_init(&s->comm, uid, world, rank, err);
-    if (st != SV_OK) {
-        free_state(s);
-        return fail(st, err);
-    }
-    // staging buffer for the chunked exchange: 1/world of the shard (one peer chunk)
-    s->xbuf_bytes = bytes / world;
-    e = cudaMalloc(&s->xbuf, s->xbuf_bytes);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        free_state(s);
-        return fail(SV_ERR_RESOURCE, "cannot allocate the exchange buffer (" + std::to_string(bytes / world) + " bytes)");
+    if (ctl) {
+        s->host_ctl = true;
+        s->ctl = *ctl;
+    } else {
+        st = comm_init(&s->comm, uid, world, rank, err);
+        if (st != SV_OK) {
+            free_state(s);
+            return fail(st, err);
+        }
+        // staging buffer of the NCCL exchange (fallback / exchange = 1): at most 1 GiB; the
+        // chunks go through it piece by piece, so 35-36 q shards fit next to it
+        s->xbuf_bytes = std::min<size_t>(bytes / world, (size_t)1 << 30);
+        cudaError_t e = cudaMalloc(&s->xbuf, s->xbuf_bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            free_state(s);
+            return fail(SV_ERR_RESOURCE, "cannot allocate the exchange buffer (" + std::to_string(s->xbuf_bytes) + " bytes)");
+        }
     }
     st = sv_init_zero(s);
     if (st != SV_OK) {
@@ -401,6 +451,12 @@ sv_status sv_create_sharded(int n, sv_dtype dtype, const void* uid, int world, i
     }
     *out = s;
     return SV_OK;
+}
+
+sv_status sv_create_sharded(int n, sv_dtype dtype, const void* uid, int world, int rank, void* stream,
+                            sv_state* out) {
+    if (!uid) return fail(SV_ERR_ARG, "NULL argument");
+    return sv_create_sharded_ex(n, dtype, uid, nullptr, world, rank, nullptr, stream, out);
 }
 
 sv_status sv_destroy(sv_state s) {
@@ -492,7 +548,7 @@ sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts
     if (!out || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
     if (!valid_dtype(dtype)) return fail(SV_ERR_ARG, "bad dtype");
     if (opts && (opts->force_kernel < 0 || opts->force_kernel > 3 || opts->tile_qubits < 0 || opts->exchange < 0 ||
-                 opts->exchange > 1))
+                 opts->exchange > 1 || opts->max_fused_k != 0))
         return fail(SV_ERR_ARG, "bad sv_run_opts");
     auto* p = new sv_plan_s();
     std::string err;
@@ -623,11 +679,15 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
     // fused init: a deferred basis state is synthesised by the first pass instead of written
     int64_t kb = -1;
     bool unif = false;
-    if (s->lazy_basis >= 0 && !p->opts.use_graph && !p->sched.passes.empty() && p->sched.passes[0].jit_fn_basis) {
+    const bool basis_variant = !p->sched.passes.empty() &&
+                               (p->sched.passes[0].jit_fn_basis || p->sched.passes[0].pair_fn_basis);
+    const bool unif_variant = !p->sched.passes.empty() &&
+                              (p->sched.passes[0].jit_fn_unif || p->sched.passes[0].pair_fn_unif);
+    if (s->lazy_basis >= 0 && !p->opts.use_graph && basis_variant) {
         kb = s->lazy_basis;
         s->lazy_basis = -1;  // the map is the identity after an init
     }
-    if (s->lazy_uniform && !p->opts.use_graph && !p->sched.passes.empty() && p->sched.passes[0].jit_fn_unif) {
+    if (s->lazy_uniform && !p->opts.use_graph && unif_variant) {
         unif = true;
         s->lazy_uniform = false;
     }
@@ -672,6 +732,10 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
         p->prof_n = p->opts.profile ? (int)p->sched.passes.size() : 0;
     }
     if (st == SV_OK && !p->sched.end_phys.empty()) s->phys = p->sched.end_phys;  // layout-changing plan
+    // A borrowed buffer (sv_wrap) is the caller's tensor: it must hold the state in logical
+    // index order once the call's work completes, so a relabelling plan's final
+    // layout is undone here (one more tile pass of physical SWAPs, only for such plans).
+    if (st == SV_OK && !s->owned) st = canonicalize(s);
     if (stats) stats->gates = p->circ.gates.size();
     return st;
 }
@@ -679,37 +743,48 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
 sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* opts, sv_run_stats* stats) {
     if (!s || !ir_text) return fail(SV_ERR_ARG, "NULL argument");
     const auto t0 = std::chrono::steady_clock::now();
-    // process-wide plan cache keyed by (dtype, options, IR text): a circuit that is run again
-    // skips parsing, planning and code generation (SURVEY 8(b) plan_cache)
+    // process-wide plan cache keyed by (device, world, dtype, options, IR text): a circuit that
+    // is run again skips parsing, planning and code generation (SURVEY 8(b) plan_cache).  The
+    // device is part of the key (generated kernels carry per-device function attributes).
+    // Entries are shared_ptrs: a caller keeps its plan alive for the whole call even if
+    // another thread evicts it, and the plan's own mutex serialises applies that share it
+    // (jit state, shard cache and profiling events are per plan).
+    using PlanRef = std::shared_ptr<sv_plan_s>;
     static std::mutex mu;
-    static std::list<std::pair<std::string, sv_plan_s*>> cache;
-    std::string key(reinterpret_cast<const char*>(&s->dtype), sizeof(s->dtype));
+    static std::list<std::pair<std::string, PlanRef>> cache;
+    std::string key;
+    key.append(reinterpret_cast<const char*>(&s->device), sizeof(s->device));
+    key.append(reinterpret_cast<const char*>(&s->world), sizeof(s->world));
+    key.append(reinterpret_cast<const char*>(&s->dtype), sizeof(s->dtype));
     sv_run_opts o{};
     if (opts) o = *opts;
     key.append(reinterpret_cast<const char*>(&o), sizeof(o));
     key.append(ir_text);
-    sv_plan p = nullptr;
+    PlanRef p;
     {
         std::lock_guard<std::mutex> lk(mu);
-        for (auto& kv : cache)
-            if (kv.first == key) {
-                p = kv.second;
+        for (auto it = cache.begin(); it != cache.end(); ++it)
+            if (it->first == key) {
+                p = it->second;
+                cache.splice(cache.begin(), cache, it);  // most recently used first
                 break;
             }
     }
     sv_status st = SV_OK;
     if (!p) {
-        st = sv_plan_compile(ir_text, s->dtype, opts, &p);
+        sv_plan raw = nullptr;
+        st = sv_plan_compile(ir_text, s->dtype, opts, &raw);
         if (st != SV_OK) return st;
+        p = PlanRef(raw, [](sv_plan_s* q) { sv_plan_destroy(q); });
         std::lock_guard<std::mutex> lk(mu);
         cache.emplace_front(key, p);
-        while (cache.size() > 16) {
-            sv_plan_destroy(cache.back().second);
-            cache.pop_back();
-        }
+        while (cache.size() > 16) cache.pop_back();  // destroyed when its last user returns
     }
     if (p->circ.n != s->n) return fail(SV_ERR_STATE, "circuit width does not match the state");
-    st = sv_plan_apply(s, p, stats);
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        st = sv_plan_apply(s, p.get(), stats);
+    }
     const auto t1 = std::chrono::steady_clock::now();
     if (stats) stats->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     return st;
@@ -879,11 +954,12 @@ sv_status sv_info(sv_state s, int* n, int* n_local, int* world, int* rank, sv_dt
 }
 
 sv_status sv_device_ptr(sv_state s, void** dev_ptr, uint64_t* local_amps) {
-    if (s) {
-        const sv_status st = materialize(s);
+    if (!s) return fail(SV_ERR_ARG, "NULL state");
+    {
+        // the buffer handed out holds the logical state in index order
+        const sv_status st = canonicalize(s);
         if (st != SV_OK) return st;
     }
-    if (!s) return fail(SV_ERR_ARG, "NULL state");
     if (dev_ptr) *dev_ptr = s->d;
     if (local_amps) *local_amps = s->virt ? (1ull << s->n) : s->local_amps();
     return SV_OK;

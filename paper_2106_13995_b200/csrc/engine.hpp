@@ -136,6 +136,17 @@ struct PassPlan {
     uint64_t ntiles = 0, groups = 0;
     int nops = 0;
     uint64_t touched_amps = 0;           // amplitudes read and written (algorithmic bytes / 2 / amp size)
+    // Pass pair through L2 (jit.cpp gen_pair_source): this pass and the next one run as ONE
+    // persistent kernel, chunk by chunk, the second reading the first's output from L2.
+    // Set on the first pass of the pair; the second has paired_second = true.
+    void* pair_fn = nullptr;
+    void* pair_fn_basis = nullptr;
+    void* pair_fn_unif = nullptr;
+    bool paired_second = false;
+    int pair_threads = 0;
+    size_t pair_smem = 0;
+    unsigned pair_grid = 0;
+    uint64_t pair_chunks = 0;            // chunk counters the kernel needs (+1 ticket word)
     std::vector<unsigned char> params;   // PassParams<real> or DenseParams<real> bytes
 };
 

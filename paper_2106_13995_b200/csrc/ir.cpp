@@ -145,6 +145,12 @@ sv_status parse_ir(const char* text, Circuit& out, std::string& err) {
                 err = "line " + std::to_string(line) + ": bad qubit count";
                 return SV_ERR_PARSE;
             }
+            // one header, before any gate: gates are range-checked against the n in force
+            // when they are parsed, so a later (smaller) header would leave them out of range
+            if (out.n >= 0) {
+                err = "line " + std::to_string(line) + ": repeated 'qubits:' header";
+                return SV_ERR_PARSE;
+            }
             out.n = (int)n;
             continue;
         }

@@ -821,20 +821,22 @@ std::string deposit_expr(const std::vector<int>& dst, bool wide) {
 }  // namespace
 
 std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, size_t& smem, bool& persistent,
-                            int& tpc, bool basis_in, int xS, bool uniform_in, cd carry_in, cd* carry_out) {
+                            int& tpc, bool basis_in, int xS, bool uniform_in, cd carry_in, cd* carry_out,
+                            const GenMode* mode) {
     Em e;
     e.dbl = sym.dbl;
+    const GenMode md = mode ? *mode : GenMode();
     const int rb = sym.rb, R = 1 << rb;
     const int m = (int)sym.tq.size();
     const int tb = m - rb;
     const int tthreads = 1 << tb;  // threads per tile
     const bool multi = sym.stages.size() > 1;
-    const bool pf = !basis_in && !uniform_in && xS < 0 && prefetch_enabled() && m >= (sym.dbl ? 4 : 5) + 1 &&
-                    ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)tthreads == 0;
+    const bool pf = !md.device_fn && !basis_in && !uniform_in && xS < 0 && prefetch_enabled() &&
+                    m >= (sym.dbl ? 4 : 5) + 1 && ((1ull << m) / (sym.dbl ? 1 : 2)) % (uint64_t)tthreads == 0;
     persistent = pf;
     const size_t tile_bytes = ((size_t)1 << m) * (sym.dbl ? 16 : 8);
     tpc = 1;
-    if (!pf)
+    if (!pf && !md.device_fn)
         while (tpc * 2 <= tiles_per_cta() && ntiles % (uint64_t)(tpc * 2) == 0 && tthreads * tpc * 2 <= 1024 &&
                (!multi || tile_bytes * tpc * 2 <= (size_t)200 * 1024))
             tpc *= 2;
@@ -846,7 +848,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
 
     auto& o = e.o;
     o << "// generated tile pass: m=" << m << " rb=" << rb << " stages=" << sym.stages.size() << "\n";
-    if (sym.dbl) {
+    if (!md.prelude) {
+    } else if (sym.dbl) {
         o << "typedef double R;\n";
         o << "struct alignas(16) C { R x, y; };\n";
         o << "__device__ __forceinline__ C mk(R x, R y){C c; c.x=x; c.y=y; return c;}\n";
@@ -871,6 +874,14 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes
         o << (scalar_fma() ? "#define F F1\n" : "#define F F2\n");
     }
+    if (md.prelude && md.ldcg) {
+        // loads of a paired pass go to L2 only (ld.global.cg): the second pass of a pair reads
+        // what other SMs wrote in the same kernel, which this SM's L1 may hold stale
+        if (sym.dbl)
+            o << "__device__ __forceinline__ C LDG(const C* p){const double2 d=__ldcg((const double2*)p);return mk(d.x,d.y);}\n";
+        else
+            o << "#define LDG(p) __ldcg((const unsigned long long*)(p))\n";
+    }
     // pf: persistent CTAs; the next tile is prefetched into the second shared-memory buffer
     // with cp.async while this one is computed (HBM reads overlap the arithmetic)
     const uint32_t smask = swz_mask(sym.dbl, pf);
@@ -880,6 +891,14 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     // xS >= 0: fused exchange -- the pass stores every amplitude straight to
     // where the global<->local swap puts it: local index a on rank r (top local bits c = a >> xS)
     // goes to rank c at (a & (2^xS - 1)) | r << xS, through the peers' second buffers
+    if (md.device_fn) {
+        // one tile of the pass as a device function (pair kernels): the caller passes the
+        // tile's physical base index and the shared-memory tile buffer
+        o << "__device__ __forceinline__ void " << md.fname << "(C* __restrict__ psi,const unsigned long long base,C* sm"
+          << (basis_in ? ",const unsigned long long kb" : "") << (uniform_in ? ",const C u0" : "") << "){\n";
+        o << "const unsigned t=threadIdx.x;\n";
+        o << "C v[" << R << "];\nunsigned long long g;\n";
+    } else {
     if (xS >= 0) o << "struct XT { C* p[8]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
       << (pf ? std::max(1, min_blocks(threads, sym.dbl) / 2) : min_blocks(threads, sym.dbl)) << ") svpass(C* __restrict__ psi"
@@ -891,6 +910,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (tpc > 1) o << "const unsigned t=threadIdx.x&" << (tthreads - 1) << "u;\n";
     else o << "const unsigned t=threadIdx.x;\n";
     o << "C v[" << R << "];\nunsigned long long g,base;\n";
+    }
     if (multi || pf) o << "unsigned tl,tr,tw;\n";
     const int L = sym.dbl ? 4 : 5;  // the tile's low qubits 0..L-1 are contiguous in memory
     if (pf) {
@@ -930,14 +950,15 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         o << "{const unsigned long long nt=tile+gridDim.x; if(nt<NT) PF(nt,bn); asm volatile(\"cp.async.commit_group;\");}\n";
         o << "asm volatile(\"cp.async.wait_group 1;\"); __syncthreads();\n";
         o << "base=tile;\n";
-    } else {
+    } else if (!md.device_fn) {
         if (tpc > 1) o << "base=(unsigned long long)blockIdx.x*" << tpc << "u+(threadIdx.x>>" << tb << ");\n";
         else o << "base=blockIdx.x;\n";
     }
-    for (int b = 0; b < m; ++b) {
-        const int q = sym.tq[b];
-        o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
-    }
+    if (!md.device_fn)
+        for (int b = 0; b < m; ++b) {
+            const int q = sym.tq[b];
+            o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
+        }
     const std::string SM = pf ? "bc" : "sm";
     PassState ps;
     ps.fac = carry_in;  // global phase left pending by the previous pass of the schedule
@@ -1086,7 +1107,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             for (int s = 0; s < R; ++s) o << reg(s) << "=u0;";
             o << "\n";
         } else if (!reads_smem) {
-            for (int s = 0; s < R; ++s) o << reg(s) << "=psi[g+" << goff[s] << "ull];";
+            for (int s = 0; s < R; ++s)
+                o << reg(s) << (md.ldcg ? "=LDG(psi+g+" : "=psi[g+") << goff[s] << (md.ldcg ? "ull);" : "ull];");
             o << "\n";
         } else {
             if (si > first) o << "__syncthreads();\n";
@@ -1220,6 +1242,121 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (pf) o << "__syncthreads(); {C* tmp=bc; bc=bn; bn=tmp;}\n}\n";
     o << "}\n";
     return o.str();
+}
+
+// ------------------------------------------------------------------ pass pairs through L2
+// Two consecutive tile passes A, B of one GPU's schedule as ONE persistent kernel.  Every
+// tile of A reads and writes the physical positions S_A, every tile of B the positions S_B;
+// both contain the low (coalescing) positions, so U = S_A u S_B has at most
+// 5 + 2 (m - 5) qubits (19 for complex64 at m = 12).  Fixing the bits outside U splits the
+// state into independent chunks of 2^|U| amplitudes (4 MiB): the chunk's A tiles (indexed
+// by the bits of S_B \ S_A) must all finish before its B tiles (indexed by S_A \ S_B) start,
+// and nothing else touches the chunk.  The kernel is persistent (grid = the resident CTA
+// count) and deals work items round-robin in blocks of about one wave of A tiles, each
+// block followed by the previous block's B tiles: at any time nearly every CTA of an SM runs
+// the same pass's code (one instruction footprint), a B item waits on A items dealt a block
+// earlier (rarely still running), and it reads its chunk from L2 (in flight: ~2 blocks,
+// ~50 MB of the 126 MB L2).  HBM traffic of the pair: one read and one write of the state
+// instead of two of each.
+struct PairGeom {
+    std::vector<int> U, BmA, AmB;
+    uint64_t nch = 0, NA = 0, NB = 0;
+};
+
+PairGeom pair_geom(const TileSym& a, const TileSym& b, int nl) {
+    PairGeom g;
+    std::set<int> sa(a.tq.begin(), a.tq.end()), sb(b.tq.begin(), b.tq.end());
+    std::set<int> u = sa;
+    u.insert(sb.begin(), sb.end());
+    g.U.assign(u.begin(), u.end());
+    for (int q : sb) if (!sa.count(q)) g.BmA.push_back(q);
+    for (int q : sa) if (!sb.count(q)) g.AmB.push_back(q);
+    g.nch = 1ull << (nl - (int)g.U.size());
+    g.NA = 1ull << g.BmA.size();
+    g.NB = 1ull << g.AmB.size();
+    return g;
+}
+
+std::string gen_pair_source(const PassPlan& A, const PassPlan& B, const PairGeom& geo, int variant, int& threads,
+                            size_t& smem) {
+    int thA, thB, tpc;
+    size_t smA = 0, smB = 0;
+    bool pers;
+    GenMode ma, mb;
+    ma.device_fn = mb.device_fn = true;
+    ma.ldcg = mb.ldcg = true;
+    ma.fname = "tileA";
+    mb.fname = "tileB";
+    mb.prelude = false;
+    cd oa, ob;
+    std::string src = gen_pass_source(*A.sym, A.ntiles, thA, smA, pers, tpc, variant == 1, -1, variant == 2, A.carry_in,
+                                      A.carry_next ? &oa : nullptr, &ma);
+    src += gen_pass_source(*B.sym, B.ntiles, thB, smB, pers, tpc, false, -1, false, B.carry_in,
+                           B.carry_next ? &ob : nullptr, &mb);
+    threads = thA;
+    smem = std::max<size_t>(std::max(smA, smB), 16);
+    const bool dbl = A.sym->dbl;
+    std::ostringstream o;
+    auto deposit = [&](const std::vector<int>& pos, const char* var) {
+        // sum_i bit_i(var) << pos[i]
+        std::ostringstream t;
+        t << "0ull";
+        for (size_t i = 0; i < pos.size(); ++i) t << "|(((" << var << ">>" << i << ")&1ull)<<" << pos[i] << ")";
+        return t.str();
+    };
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << "," << min_blocks(threads, dbl)
+      << ") svpass(C* __restrict__ psi,unsigned long long* __restrict__ ctl,const unsigned long long D,"
+         "const unsigned long long LK"
+      << (variant == 1 ? ",const unsigned long long kb" : "") << (variant == 2 ? ",const C u0" : "") << "){\n";
+    o << "extern __shared__ C sm[];\n";
+    o << "unsigned* done=(unsigned*)(ctl+1);\n";
+    o << "const unsigned long long NCH=" << geo.nch << "ull,NA=" << geo.NA << "ull,NB=" << geo.NB << "ull;\n";
+    // D = chunks per block (a power of two dividing NCH).  Ticket order: A items of block 0,
+    // then for k = 0, 1, ...: A items of block k+1, B items of block k.  A block holds about
+    // one wave of tiles, so at any time nearly every CTA runs the same pass's code (one
+    // instruction footprint per SM) and a block's A tiles finished one block earlier.
+    // LK = look-ahead in blocks: A blocks 0..LK-1 first, then [A block k+LK, B block k]
+    o << "const unsigned long long BA=D*NA, BB=D*NB, NBLK=NCH/D, TOT=NCH*(NA+NB);\n";
+    o << "const unsigned long long L0=(LK<NBLK?LK:NBLK), P0=L0*BA, K=NBLK-L0, KF=K*(BA+BB);\n";
+    o << "__shared__ unsigned long long it_s;\n";
+    // items are taken from one atomic ticket by running CTAs, in order: every A item a B item
+    // waits on was taken earlier by a running CTA, so it completes whatever the residency
+    o << "for(;;){\n";
+    o << "if(threadIdx.x==0) it_s=atomicAdd(ctl,1ull);\n__syncthreads();\n";
+    o << "const unsigned long long it=it_s;\n__syncthreads();\n";
+    o << "if(it>=TOT) break;\n";
+    o << "unsigned long long c,j; bool isA;\n";
+    o << "if(it<P0){isA=true;c=it/NA;j=it%NA;}\n";
+    o << "else{unsigned long long i2=it-P0;\n"
+         " if(i2<KF){const unsigned long long k=i2/(BA+BB), r=i2%(BA+BB);\n"
+         "  if(r<BA){isA=true;c=(k+L0)*D+r/NA;j=r%NA;}else{isA=false;c=k*D+(r-BA)/NB;j=(r-BA)%NB;}}\n"
+         " else{i2-=KF;isA=false;c=K*D+i2/NB;j=i2%NB;}}\n";
+    o << "unsigned long long base=c;\n";
+    for (int q : geo.U) o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
+    o << "if(isA){\n";
+    o << "tileA(psi,base|(" << deposit(geo.BmA, "j") << "),sm" << (variant == 1 ? ",kb" : "") << (variant == 2 ? ",u0" : "")
+      << ");\n";
+    o << "__syncthreads();\nif(threadIdx.x==0){__threadfence();atomicAdd(done+c,1u);}\n";  // (RED: no wait)
+    o << "}else{\n";
+    o << "if(threadIdx.x==0){unsigned v;for(;;){asm volatile(\"ld.acquire.gpu.global.u32 %0,[%1];\":\"=r\"(v):\"l\"(done+c):\"memory\");"
+         "if(v>=NA)break;__nanosleep(64);}__threadfence();}\n";
+    o << "__syncthreads();\n";
+    o << "tileB(psi,base|(" << deposit(geo.AmB, "j") << "),sm);\n";
+    o << "}\n}\n}\n";
+    return src + o.str();
+}
+
+// Measured on B200 (profiles/r02_pair.txt): slower than the two passes it replaces (30 q
+// c64 pairs (0,1) 8.3 vs 7.26 ms, (4,5) 6.9 vs 5.9 ms).  With blocks of about a wave the
+// second pass misses L2 entirely (DRAM bytes = two passes' worth); with blocks small enough
+// that it hits (DRAM = one pass's worth, ~1/20 wave) the chunk barriers serialise the
+// machine (8.7 ms).  Off by default; SV_PAIR=1 turns it on (ablation).
+bool pair_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_PAIR");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
 }
 
 // ------------------------------------------------------------------ compile + cache
@@ -1409,17 +1546,61 @@ static sv_status jit_prepare_x(Schedule& sc, std::string& err) {
 }
 
 sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
+    // pass pairs through L2 (single-GPU schedules): consecutive generated tile passes of the
+    // same CTA shape whose union of tile positions gives chunks of <= 8 MiB
+    struct PairJob {
+        size_t a;
+        PairGeom geo;
+        int variant;
+        std::string src;
+        int threads = 0;
+        size_t smem = 0;
+        void* fn = nullptr;
+        sv_status st = SV_OK;
+        std::string err;
+    };
+    std::vector<PairJob> pjobs;
+    if (with_basis && pair_enabled()) {
+        jit_carries(sc);
+        for (size_t i = 0; i + 1 < sc.passes.size(); ++i) {
+            PassPlan &A = sc.passes[i], &B = sc.passes[i + 1];
+            auto gen_ok = [](const PassPlan& x) {
+                return x.kind == PassPlan::TILE && x.sym && x.xS < 0 && !x.jit_persistent && !x.pair_fn &&
+                       !x.paired_second && x.ntiles > 0;
+            };
+            if (!gen_ok(A) || !gen_ok(B) || A.sym->dbl != B.sym->dbl) continue;
+            if ((int)A.sym->tq.size() - A.sym->rb != (int)B.sym->tq.size() - B.sym->rb) continue;  // same CTA size
+            int nl = (int)A.sym->tq.size();
+            while ((1ull << (nl - (int)A.sym->tq.size())) < A.ntiles) ++nl;
+            const PairGeom geo = pair_geom(*A.sym, *B.sym, nl);
+            const size_t chunk_bytes = ((size_t)1 << geo.U.size()) * (A.sym->dbl ? 16 : 8);
+            if (geo.BmA.empty() || geo.AmB.empty() || chunk_bytes > ((size_t)8 << 20) || geo.nch < 8) continue;
+            for (int v = 0; v < (i == 0 ? 3 : 1); ++v) pjobs.push_back(PairJob{i, geo, v, std::string()});
+            B.paired_second = true;
+            A.pair_chunks = geo.nch;
+            ++i;  // B is taken
+        }
+    }
+    auto paired = [&](const PassPlan& pp) {
+        if (pp.paired_second) return true;
+        for (const PairJob& j : pjobs)
+            if (&sc.passes[j.a] == &pp) return true;
+        return false;
+    };
     std::vector<PassPlan*> todo;
     for (PassPlan& pp : sc.passes)
-        if (((pp.kind == PassPlan::TILE && pp.sym) || pp.kind == PassPlan::PERM) && !pp.jit_fn) todo.push_back(&pp);
+        if (((pp.kind == PassPlan::TILE && pp.sym) || pp.kind == PassPlan::PERM) && !pp.jit_fn && !paired(pp))
+            todo.push_back(&pp);
     // the first pass, if a generated tile pass, also gets its basis-input variant (fused init)
     PassPlan* first = (with_basis && !sc.passes.empty() && sc.passes[0].kind == PassPlan::TILE && sc.passes[0].sym &&
-                       !sc.passes[0].jit_fn_basis)
+                       !sc.passes[0].jit_fn_basis && !paired(sc.passes[0]))
                           ? &sc.passes[0]
                           : nullptr;
-    if (todo.empty() && !first) return jit_prepare_x(sc, err);
+    if (todo.empty() && !first && pjobs.empty()) return jit_prepare_x(sc, err);
     std::vector<std::string> srcs(todo.size() + (first ? 1 : 0));
     jit_carries(sc);
+    for (PairJob& j : pjobs)
+        j.src = gen_pair_source(sc.passes[j.a], sc.passes[j.a + 1], j.geo, j.variant, j.threads, j.smem);
     for (size_t i = 0; i < todo.size(); ++i) {
         if (todo[i]->kind == PassPlan::PERM) {
             srcs[i] = gen_perm_source(*todo[i], todo[i]->perm_dbl, todo[i]->jit_threads);
@@ -1450,18 +1631,25 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
                                        first->carry_in, first->carry_next ? &o2 : nullptr));
     }
     const size_t nsrc = srcs.size();
+    const size_t njobs = nsrc + pjobs.size();
     std::vector<sv_status> st(nsrc, SV_OK);
     std::vector<std::string> errs(nsrc);
     std::vector<void*> fns(nsrc, nullptr);
     int dev = 0;
     cudaGetDevice(&dev);
-    const size_t nthr = std::max<size_t>(1, std::min<size_t>(nsrc, std::thread::hardware_concurrency()));
+    const size_t nthr = std::max<size_t>(1, std::min<size_t>(njobs, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
     for (size_t w = 0; w < nthr; ++w)
         pool.emplace_back([&, w]() {
             cudaSetDevice(dev);
-            for (size_t i = w; i < nsrc; i += nthr)
-                st[i] = jit_compile(srcs[i], i < todo.size() ? todo[i]->jit_smem : basis_smem, &fns[i], errs[i]);  // the two input variants share the pass's shared-memory size
+            for (size_t i = w; i < njobs; i += nthr) {
+                if (i < nsrc)
+                    st[i] = jit_compile(srcs[i], i < todo.size() ? todo[i]->jit_smem : basis_smem, &fns[i], errs[i]);  // the two input variants share the pass's shared-memory size
+                else {
+                    PairJob& j = pjobs[i - nsrc];
+                    j.st = jit_compile(j.src, j.smem, &j.fn, j.err);
+                }
+            }
         });
     for (auto& th : pool) th.join();
     for (size_t i = 0; i < nsrc; ++i)
@@ -1469,6 +1657,22 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
             err = errs[i];
             return st[i];
         }
+    for (PairJob& j : pjobs) {
+        if (j.st != SV_OK) {
+            err = j.err;
+            return j.st;
+        }
+        PassPlan& A = sc.passes[j.a];
+        (j.variant == 0 ? A.pair_fn : j.variant == 1 ? A.pair_fn_basis : A.pair_fn_unif) = j.fn;
+        if (j.variant == 0) {
+            int per_sm = 0, nsm = 148;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)j.fn, j.threads, j.smem);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            A.pair_threads = j.threads;
+            A.pair_smem = j.smem;
+            A.pair_grid = (unsigned)std::max(1, per_sm) * (unsigned)nsm;
+        }
+    }
     if (first) {
         first->jit_fn_basis = fns[todo.size()];
         first->jit_fn_unif = fns[todo.size() + 1];
@@ -1519,6 +1723,41 @@ cudaError_t jit_launch_uniform(const PassPlan& pp, void* psi, double amp, bool d
     void* args[] = {&psi, dbl ? (void*)&u2 : (void*)&u1};
     return cudaLaunchKernel(pp.jit_fn_unif, dim3(pp.jit_grid), dim3((unsigned)pp.jit_threads), args, pp.jit_smem,
                             stream);
+}
+
+cudaError_t jit_launch_pair(const PassPlan& pp, void* psi, void* ctl, int variant, uint64_t kb, double amp,
+                            cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(ctl, 0, (size_t)(pp.pair_chunks + 1) * 8, stream);
+    if (e != cudaSuccess) return e;
+    // look-ahead: enough A items ahead of the B items that every resident CTA has work
+    // before the first B item (whose chunk then has long finished)
+    const uint64_t na = std::max<uint64_t>(1, pp.ntiles / std::max<uint64_t>(1, pp.pair_chunks));  // A tiles per chunk
+    // chunks per block: the power of two nearest to (SV_PAIR_WAVES x resident CTAs) / NA tiles
+    static const double waves = [] {
+        const char* e = getenv("SV_PAIR_WAVES");
+        return e ? atof(e) : 1.0;
+    }();
+    const double want = std::max(1.0, waves * pp.pair_grid / (double)na);
+    unsigned long long D = 1;
+    while (D * 2 <= pp.pair_chunks && (double)(D * 2) <= want * 1.41) D *= 2;
+    void* fn = variant == 1 ? pp.pair_fn_basis : variant == 2 ? pp.pair_fn_unif : pp.pair_fn;
+    unsigned long long k = kb;
+    struct alignas(16) C2 {
+        double x, y;
+    } u2{amp, 0.0};
+    unsigned long long u1;
+    const float f[2] = {(float)amp, 0.0f};
+    std::memcpy(&u1, f, 8);
+    static const unsigned long long look = [] {
+        const char* e = getenv("SV_PAIR_LOOK");
+        return (unsigned long long)(e ? std::max(1, atoi(e)) : 2);
+    }();
+    unsigned long long LK = look;
+    void* args1[] = {&psi, &ctl, &D, &LK};
+    void* args2[] = {&psi, &ctl, &D, &LK, &k};
+    void* args3[] = {&psi, &ctl, &D, &LK, pp.sym->dbl ? (void*)&u2 : (void*)&u1};
+    void** args = variant == 1 ? args2 : variant == 2 ? args3 : args1;
+    return cudaLaunchKernel(fn, dim3(pp.pair_grid), dim3((unsigned)pp.pair_threads), args, pp.pair_smem, stream);
 }
 
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {

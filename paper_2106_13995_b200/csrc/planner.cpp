@@ -61,7 +61,11 @@ bool unit_factor(const std::vector<cd>& U, std::vector<cd>& V, cd& f) {
     if (f == cd(0, 0)) return false;
     V.resize(U.size());
     static const cd units[4] = {cd(1, 0), cd(-1, 0), cd(0, 1), cd(0, -1)};
-    const double tol = 1e-12 * std::abs(f);
+    // a few ulp of |f| (16 ulp = 2^-48 |f| ~ 3.6e-15 |f|): enough for the rounding of the
+    // named gates' entries and of one 2x2 product (merged runs are re-snapped after every
+    // product, merge_single_qubit), small enough that a user's deliberate deviation from a
+    // unit-class matrix (1e-13 and up) is kept (DESIGN reading "unit-class snap")
+    const double tol = 0x1p-48 * std::abs(f);
     for (size_t i = 0; i < U.size(); ++i) {
         if (std::abs(U[i]) <= tol) { V[i] = 0; continue; }
         bool hit = false;
@@ -108,6 +112,13 @@ Circuit merge_single_qubit(const Circuit& c) {
                 std::vector<cd> P(4);
                 for (int r = 0; r < 2; ++r)
                     for (int cc = 0; cc < 2; ++cc) P[r * 2 + cc] = g.U[r * 2] * A[cc] + g.U[r * 2 + 1] * A[2 + cc];
+                // the exact product of two unit-class matrices is unit class; snap away the
+                // rounding of this product (f * V with V in {0, +-1, +-i} is exact) so that
+                // the rounding does not accumulate along a long run
+                std::vector<cd> PV;
+                cd pf;
+                if (unit_factor(P, PV, pf))
+                    for (int i = 0; i < 4; ++i) P[i] = pf * PV[i];
                 if (late) {
                     out.gates[j].U.clear();  // dropped below; the product takes the later place
                     Gate m = g;

@@ -56,7 +56,7 @@ sv_status peer_setup(sv_state_s* s, std::string& err) {
     if (s->xmode) return SV_OK;
     const size_t shard = (size_t)s->local_amps() * s->amp_bytes();
     const size_t bytes = s->virt ? shard * s->world : shard;
-    bool ok = s->world <= 8 && s->owned;
+    bool ok = s->world <= 8;
     if (ok && !s->d2) {
         if (cudaMalloc(&s->d2, bytes) != cudaSuccess) {
             cudaGetLastError();
@@ -126,6 +126,12 @@ sv_status peer_setup(sv_state_s* s, std::string& err) {
     }
     s->xmode = all_ok ? 1 : 2;
     s->xcur = 0;
+    if (!all_ok && s->host_ctl) {
+        // no NCCL transport behind a host control plane
+        err = "peer-memory exchange unavailable on some rank (second shard buffer or CUDA IPC mapping failed) "
+              "and a host control plane has no NCCL fallback";
+        return SV_ERR_RESOURCE;
+    }
     return SV_OK;
 }
 
@@ -147,14 +153,14 @@ sv_status peer_flip(sv_state_s* s, sv_run_stats* st, std::string& err) {
 // launch one shard's schedule; outs != null: the schedule feeds a fused exchange -- its last
 // pass stores into the peers' second buffers (or, if it cannot, a peer copy follows)
 sv_status run_sched(sv_state_s* s, int i, const Schedule& sc, sv_run_stats* st, std::string& err,
-                    void* const* outs = nullptr) {
+                    void* const* outs = nullptr, bool fused = true) {
     void* psi = s->shard_ptr(i);
     const unsigned rank = (unsigned)rank_of(s, i);
     bool stored = false;
     for (size_t pi = 0; pi < sc.passes.size(); ++pi) {
         const PassPlan& pp = sc.passes[pi];
         const bool last = pi + 1 == sc.passes.size();
-        if (outs && last && pp.jit_fn_x) {
+        if (outs && fused && last && pp.jit_fn_x) {
             const cudaError_t e = jit_launch_x(pp, psi, outs, rank, s->stream);
             if (e != cudaSuccess) {
                 err = std::string("fused exchange pass launch: ") + cudaGetErrorString(e);
@@ -251,14 +257,20 @@ sv_status exchange_all(sv_state_s* s, sv_run_stats* st, std::string& err) {
                 }
             }
     } else {
+        // pairwise with every peer, through the staging buffer piece by piece (the buffer is
+        // at most 1 GiB, so it fits next to a 128 GiB shard)
+        const size_t piece = std::min(chunk, s->xbuf_bytes);
         for (int k = 1; k < P; ++k) {
             const int peer = s->rank ^ k;
             char* mine = (char*)s->d + (size_t)peer * chunk;
-            sv_status r = comm_sendrecv(s, peer, mine, s->xbuf, chunk, err);
-            if (r != SV_OK) return r;
-            if (cudaMemcpyAsync(mine, s->xbuf, chunk, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
-                err = "exchange unpack copy failed";
-                return SV_ERR_CUDA;
+            for (size_t off = 0; off < chunk; off += piece) {
+                const size_t len = std::min(piece, chunk - off);
+                sv_status r = comm_sendrecv(s, peer, mine + off, s->xbuf, len, err);
+                if (r != SV_OK) return r;
+                if (cudaMemcpyAsync(mine + off, s->xbuf, len, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
+                    err = "exchange unpack copy failed";
+                    return SV_ERR_CUDA;
+                }
             }
         }
     }
@@ -291,6 +303,24 @@ sv_status exchange_one(sv_state_s* s, int j, std::string& err) {
                 }
             }
         }
+    } else if (s->xmode == 1) {
+        // peer memory: push both halves into the second buffers, barrier, flip.  Rank r (bit b
+        // = bit j of r) keeps its half b (own second buffer, half b) and gives its half 1-b to
+        // the partner (partner's second buffer, half b); the second buffers are idle (their
+        // last readers finished before the previous barrier)
+        const int b = (s->rank >> j) & 1;
+        const int peer = s->rank ^ (1 << j);
+        char* mine = (char*)s->d;
+        char* own2 = (char*)s->xpeer[s->xcur ^ 1][s->rank];
+        char* peer2 = (char*)s->xpeer[s->xcur ^ 1][peer];
+        if (cudaMemcpyAsync(own2 + b * half, mine + b * half, half, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess ||
+            cudaMemcpyAsync(peer2 + b * half, mine + (1 - b) * half, half, cudaMemcpyDeviceToDevice, s->stream) !=
+                cudaSuccess) {
+            err = "peer exchange copy failed";
+            return SV_ERR_CUDA;
+        }
+        const sv_status r = peer_flip(s, nullptr, err);
+        if (r != SV_OK) return r;
     } else {
         const int b = (s->rank >> j) & 1;
         const int peer = s->rank ^ (1 << j);
@@ -328,6 +358,78 @@ uint64_t gate_mask(const Gate& g) {
     return m;
 }
 
+
+// FNV-1a signature of what every rank must agree on before the first launch of a sharded
+// plan: the circuit (gates, matrices) and the plan's collective structure (batches and
+// exchange steps, the final qubit map).  Passes inside a batch may differ by rank
+// (rank-constant folding), the sequence of collective steps may not.
+uint64_t plan_signature(const sv_plan_s* p, const ShardPlan& sp, int n) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* data, size_t len) {
+        const unsigned char* c = (const unsigned char*)data;
+        for (size_t i = 0; i < len; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    };
+    auto mixi = [&](int64_t v) { mix(&v, sizeof v); };
+    mixi(n);
+    mixi(sp.world);
+    mixi(sp.dbl);
+    mixi((int64_t)p->circ.gates.size());
+    for (const Gate& g : p->circ.gates) {
+        mixi((int64_t)g.targets.size());
+        for (int q : g.targets) mixi(q);
+        mixi((int64_t)g.controls.size());
+        for (int q : g.controls) mixi(q);
+        for (const cd& z : g.U) {
+            const double re = z.real(), im = z.imag();
+            mix(&re, sizeof re);
+            mix(&im, sizeof im);
+        }
+    }
+    mixi((int64_t)sp.steps.size());
+    for (const ShardStep& st : sp.steps) mixi(st.exchange ? 1 : 0);
+    mixi((int64_t)sp.swaps);
+    for (int q : sp.start_phys) mixi(q);
+    for (int q : sp.end_phys) mixi(q);
+    return h;
+}
+
+// Every rank compares the signatures of all ranks (one all-gather, once per cached plan);
+// a mismatch fails on every rank alike, before anything is launched.
+sv_status verify_plan(sv_state_s* s, const sv_plan_s* p, ShardPlan& sp, std::string& err) {
+    if (s->virt || sp.verified) return SV_OK;
+    const uint64_t mine = plan_signature(p, sp, s->n);
+    std::vector<unsigned char> all;
+    const sv_status r = comm_allgather_bytes(s, &mine, sizeof mine, all, err);
+    if (r != SV_OK) return r;
+    for (int c = 0; c < s->world; ++c) {
+        uint64_t other;
+        memcpy(&other, all.data() + c * sizeof other, sizeof other);
+        if (other != mine) {
+            err = "sharded plan differs between ranks (rank " + std::to_string(c) + " vs rank " +
+                  std::to_string(s->rank) + "): every rank must apply the same circuit in the same order";
+            return SV_ERR_STATE;
+        }
+    }
+    sp.verified = true;
+    return SV_OK;
+}
+
+// A borrowed shard buffer must hold the local shard when a call's work completes: if the
+// peer-memory flips left the state in the library's second buffer, copy it back and flip
+// the pair back (every rank alike), then barrier so no peer stores into that buffer before
+// the copy has read it.
+sv_status restore_borrowed(sv_state_s* s, std::string& err) {
+    if (!s->user_buf || s->virt || s->d == s->user_buf) return SV_OK;
+    const size_t bytes = (size_t)s->local_amps() * s->amp_bytes();
+    if (cudaMemcpyAsync(s->user_buf, s->d, bytes, cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess) {
+        err = "copy back into the borrowed shard buffer failed";
+        return SV_ERR_CUDA;
+    }
+    std::swap(s->d, s->d2);
+    s->xcur ^= 1;
+    return comm_barrier(s, err);
+}
+
 }  // namespace
 
 sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
@@ -347,11 +449,18 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
         p->shard_cache.push_back(std::move(plan));
         sp = &p->shard_cache.back();
     }
-    if (o.exchange == 0 && sp->swaps > 0 && !s->xmode) {
+    {
+        const sv_status r = verify_plan(s, p, *sp, err);
+        if (r != SV_OK) return set_err(r, err);
+    }
+    // a host control plane has no NCCL transport: its exchanges always go through peer
+    // memory (fused remote stores, or with exchange = 1 the peer-copy kernel)
+    if ((o.exchange == 0 || s->host_ctl) && sp->swaps > 0 && !s->xmode) {
         const sv_status r = peer_setup(s, err);
         if (r != SV_OK) return set_err(r, err);
     }
-    const bool peer = o.exchange == 0 && s->xmode == 1;
+    const bool peer = (o.exchange == 0 || s->host_ctl) && s->xmode == 1;
+    const bool fused = o.exchange == 0;
     for (size_t si = 0; si < sp->steps.size(); ++si) {
         ShardStep& step = sp->steps[si];
         sv_status r;
@@ -364,7 +473,7 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
                     r = jit_prepare(step.sched[i], err);
                     if (r != SV_OK) return set_err(r, err);
                 }
-                r = run_sched(s, (int)i, step.sched[i], stats, err, feeds ? s->xpeer[s->xcur ^ 1] : nullptr);
+                r = run_sched(s, (int)i, step.sched[i], stats, err, feeds ? s->xpeer[s->xcur ^ 1] : nullptr, fused);
                 if (r != SV_OK) return set_err(r, err);
             }
             r = SV_OK;
@@ -373,6 +482,13 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
     }
     s->phys = sp->end_phys;
     if (stats) stats->gates = p->circ.gates.size();
+    if (s->user_buf) {
+        // borrowed shard: logical order, in the caller's buffer
+        sv_status r = sharded_canonicalize(s);
+        if (r != SV_OK) return r;
+        r = restore_borrowed(s, err);
+        if (r != SV_OK) return set_err(r, err);
+    }
     return SV_OK;
 }
 
@@ -552,6 +668,12 @@ sv_status sharded_canonicalize(sv_state_s* s) {
     std::string err;
     RunOpts o;
     const int nl = s->nl, g = s->g;
+    bool global_moves = false;
+    for (int j = 0; j < g; ++j) global_moves |= s->phys[s->n - g + j] != nl + j;
+    if (global_moves && s->host_ctl && !s->virt && !s->xmode) {
+        const sv_status r = peer_setup(s, err);
+        if (r != SV_OK) return set_err(r, err);
+    }
     auto relabel = [&](const std::vector<std::pair<int, int>>& sw) -> sv_status {
         std::vector<std::vector<LOp>> ops(nshards(s));
         for (auto& pr : sw)

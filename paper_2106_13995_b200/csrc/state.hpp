@@ -2,6 +2,7 @@
 #pragma once
 #include <list>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -35,9 +36,17 @@ struct sv_state_s {
     void* xpeer[2][8] = {};
     std::vector<void*> ipc_open;  // peer mappings to close
     void* xflag = nullptr;        // 4-byte device word for the stream-ordered barrier
+    // control plane: NCCL (comm) or the caller's host callbacks (sv_control, host_ctl)
+    bool host_ctl = false;
+    sv_control ctl{};
+    void* d_gather = nullptr;     // persistent device buffer of the NCCL all-gathers
+    size_t gather_bytes = 0;
+    void* user_buf = nullptr;     // borrowed shard buffer (sharded sv_create_sharded_ex), else null
     std::vector<int> phys;  // logical qubit -> physical bit
     double* d_scratch = nullptr;
     size_t scratch_doubles = 0;
+    void* pair_ctl = nullptr;     // work ticket + chunk counters of pass-pair kernels
+    size_t pair_ctl_bytes = 0;
     int device = 0;
     // Deferred basis-state initialisation (single GPU): the state is |lazy_basis> but not yet
     // written; the first generated tile pass of the next plan synthesises its input tile instead
@@ -60,6 +69,7 @@ struct ShardStep {
 };
 
 struct ShardPlan {
+    bool verified = false;              // every rank's plan structure compared (plan_signature)
     int world = 0;
     bool dbl = false;
     std::vector<int> ranks;             // ranks whose shards this process runs
@@ -87,4 +97,5 @@ struct sv_plan_s {
     cudaGraphExec_t graph = nullptr;
     void* graph_ptr = nullptr;
     cudaStream_t graph_stream = nullptr;
+    std::mutex mu;                      // serialises applies of a plan shared through the cache
 };

@@ -18,7 +18,7 @@ template <typename real>
 struct DenseParams {
     int k;                 // target count
     int nsorted;           // |controls| + k
-    int sorted[12];        // all gate qubits ascending (bit-insertion positions)
+    int sorted[64];        // all gate qubits ascending (bit-insertion positions; up to n)
     uint64_t cmask;        // control bits (set to 1 in every group base)
     uint64_t off[32];      // offset of matrix index r: sum_j bit_j(r) << targets[j]
     real M[2 * 32 * 32];   // row-major, interleaved

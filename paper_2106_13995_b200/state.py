@@ -135,21 +135,43 @@ class StateVector:
         return cls(n, dtype, _handle=h)
 
     @classmethod
-    def sharded(cls, n: int, dtype="c64", group=None, stream=None) -> "StateVector":
-        """Collective: one process per GPU; torch.distributed broadcasts the NCCL unique id."""
+    def sharded(cls, n: int, dtype="c64", group=None, stream=None, control: str = "nccl",
+                buffer=None) -> "StateVector":
+        """Collective: one process per rank, each on its current CUDA device.
+
+        control="nccl": the library's own NCCL communicator; torch.distributed broadcasts the
+        unique id.  control="host": torch.distributed itself is the control plane (all-gather
+        + barrier callbacks, any backend incl. gloo) and every exchange goes through CUDA IPC
+        peer memory -- several ranks may then share one GPU.  buffer: optional contiguous
+        complex CUDA tensor of 2^(n - log2 world) elements to borrow as the local shard."""
         import torch.distributed as dist
 
-        from .dist import broadcast_unique_id
+        from .dist import broadcast_unique_id, host_control
         world, rank = dist.get_world_size(group), dist.get_rank(group)
-        uid = (ctypes.c_uint8 * 128)()
-        if rank == 0:
-            check(lib.sv_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p)))
-        raw = broadcast_unique_id(bytes(uid), group)
-        ctypes.memmove(uid, raw, 128)
+        ptr = None
+        if buffer is not None:
+            assert buffer.is_cuda and buffer.is_contiguous()
+            ptr = ctypes.c_void_p(buffer.data_ptr())
         h = ctypes.c_void_p()
-        check(lib.sv_create_sharded(int(n), _dtype(dtype), ctypes.cast(uid, ctypes.c_void_p), world, rank,
-                                    _stream_ptr(stream), ctypes.byref(h)))
-        return cls(n, dtype, _handle=h)
+        keep = None
+        if control == "nccl":
+            uid = (ctypes.c_uint8 * 128)()
+            if rank == 0:
+                check(lib.sv_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p)))
+            raw = broadcast_unique_id(bytes(uid), group)
+            ctypes.memmove(uid, raw, 128)
+            check(lib.sv_create_sharded_ex(int(n), _dtype(dtype), ctypes.cast(uid, ctypes.c_void_p), None, world,
+                                           rank, ptr, _stream_ptr(stream), ctypes.byref(h)))
+        elif control == "host":
+            keep = host_control(group)
+            check(lib.sv_create_sharded_ex(int(n), _dtype(dtype), None, ctypes.byref(keep), world, rank, ptr,
+                                           _stream_ptr(stream), ctypes.byref(h)))
+        else:
+            raise ValueError(f"control must be 'nccl' or 'host', not {control!r}")
+        sv = cls(n, dtype, _handle=h)
+        sv._control = keep  # the callbacks must outlive the handle
+        sv._borrowed = buffer
+        return sv
 
     # ---------------------------------------------------------------- init
     def init_zero(self):

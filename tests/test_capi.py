@@ -60,5 +60,16 @@ def test_plan_compile_parse_errors():
         P.Plan("qubits: 3\nCZ 1,1\n")
     with pytest.raises(P.SvError, match="SV_ERR_PARSE"):
         P.Plan("H 0\n")
+    # a second header after gates were range-checked against the first: rejected
+    with pytest.raises(P.SvError, match="line 4.*repeated"):
+        P.Plan("qubits: 20\nH 19\nX 18\nqubits: 2\n")
+    with pytest.raises(P.SvError, match="repeated"):
+        P.Plan("qubits: 3\nqubits: 3\nH 0\n")
+    # unused ABI slot must be zero
+    from paper_2106_13995_b200._lib import RunOpts, lib
+    import ctypes
+    h = ctypes.c_void_p()
+    o = RunOpts(1, 0, 3, 0, 0, 0, 0, 0)
+    assert lib.sv_plan_compile(b"qubits: 2\nH 0\n", 1, ctypes.byref(o), ctypes.byref(h)) == 1  # SV_ERR_ARG
     p = P.Plan("qubits: 4\nH 0; CNOT 0,1\nU 2 : 1,0,0,0,0,0,1,0\n")
     assert p.info()["gates"] == 3 and p.info()["n"] == 4

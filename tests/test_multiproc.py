@@ -51,6 +51,45 @@ def test_gloo_uid_broadcast_and_max():
         assert mx == [1.0, 10.0, 2.5]
 
 
+def _ctl_worker(rank, world, port, q):
+    import ctypes
+
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2106_13995_b200.dist import host_control
+    c = host_control()
+    # call the C function pointers exactly as libsv.so does (sv_control)
+    msg = (ctypes.c_ubyte * 5)(*[rank * 10 + i for i in range(5)])
+    out = (ctypes.c_ubyte * (5 * world))()
+    rc = c.allgather(None, ctypes.cast(msg, ctypes.c_void_p), 5, ctypes.cast(out, ctypes.c_void_p))
+    rb = c.barrier(None)
+    q.put((rank, rc, rb, bytes(out)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_control_plane_callbacks(world):
+    """The sv_control callbacks (torch.distributed over gloo) gather in rank order and
+    return 0; this is the control plane the one-GPU multi-process sharded tests use."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ctl_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = bytes(r * 10 + i for r in range(world) for i in range(5))
+    for rank, rc, rb, out in res:
+        assert rc == 0 and rb == 0
+        assert out == expect
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_shard_plan_36q_supremacy(world):
     """Config 5: 36q c64 supremacy d20 sharded over P GPUs needs one exchange step."""

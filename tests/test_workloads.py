@@ -147,6 +147,19 @@ def test_width_sweep_properties():
 def test_family_at_width():
     for n in (13, 19, 25, 28):
         assert W.family_at_width("supremacy", n).n == n
+    # the standard grids the paper names are chosen for their own widths, so the sweep
+    # takes them unchanged (golden shapes, not only widths)
+    for row in GOLDEN["supremacy_width"]:
+        assert W.supremacy_grid(row["width"]) == (row["rows"], row["cols"]), row["cite"]
+        c = W.family_at_width("supremacy", row["width"], depth=4)
+        assert c.meta.get("removed") is None and c.meta["rows"] == row["rows"] and c.meta["cols"] == row["cols"]
+    # P:63's example: a 19-qubit circuit comes from the 20-qubit one (5x4) minus one qubit
+    assert W.supremacy_grid(19) == (5, 4)
+    assert W.family_at_width("supremacy", 19, depth=4).meta["removed"] and len(
+        W.family_at_width("supremacy", 19, depth=4).meta["removed"]) == 1
+    for n in range(4, 40):
+        r, c = W.supremacy_grid(n)
+        assert r * c >= n and c <= r <= 2 * c
     for n in (13, 14, 16, 17, 21):
         c = W.family_at_width("multiplier", n)
         assert c.n == n

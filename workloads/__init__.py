@@ -28,6 +28,7 @@ from .circuits import (  # noqa: F401
     remove_random_qubit,
     width_sweep,
     family_at_width,
+    supremacy_grid,
     random_unitary,
 )
 from .states import random_state, round_to_c64  # noqa: F401

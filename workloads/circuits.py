@@ -343,17 +343,28 @@ def width_sweep(base: Circuit, min_width: int, seed: int) -> List[Circuit]:
     return out
 
 
+def supremacy_grid(n: int):
+    """The standard supremacy grid a width-n circuit is taken from: the smallest
+    near-square grid rows x cols >= n, rows >= cols, rows <= 2*cols (the paper ran square
+    n x n grids and 7 x 4; "next largest circuit"); ties on the area go to the
+    squarer grid.  25 -> 5x5, 28 -> 7x4, 36 -> 6x6, 30 -> 6x5, 19 -> 5x4 (reading in DESIGN)."""
+    best = None
+    for cols in range(1, 64):
+        for rows in range(cols, 2 * cols + 1):
+            if rows * cols < n:
+                continue
+            key = (rows * cols, rows - cols)
+            if best is None or key < best[0]:
+                best = (key, rows, cols)
+    return best[1], best[2]
+
+
 def family_at_width(family: str, n: int, seed: int = 0, depth: int = 20) -> Circuit:
     """The paper's method for non-standard widths: build the next larger standard circuit
-    and remove random qubits.  Supremacy: square-ish grids (rows x cols, rows >= cols); multiplier:
-    width 4k+1."""
+    and remove random qubits.  Supremacy: the near-square grid of supremacy_grid(n);
+    multiplier: width 4k+1."""
     if family == "supremacy":
-        best = None
-        for cols in range(2, 12):
-            for rows in range(cols, 24):
-                if rows * cols >= n and (best is None or rows * cols < best[0] * best[1]):
-                    best = (rows, cols)
-        rows, cols = best
+        rows, cols = supremacy_grid(n)
         c = supremacy(rows, cols, depth, seed)
     elif family == "multiplier":
         k = 1
