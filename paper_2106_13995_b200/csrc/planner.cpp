@@ -18,6 +18,7 @@
 // commutes gates on disjoint qubits (reading R21).  Inside a pass, gates are cut into
 // register stages of RB qubits the same way.
 #include <algorithm>
+#include <thread>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -1120,17 +1121,33 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             };
             std::vector<std::pair<double, uint64_t>> cands;  // (1-step score, low set)
             if (nt <= 20) {
+                // every L-subset of the tile qubits (Gosper's hack), scored on host threads;
+                // the best is then taken in enumeration order (the same as a sequential scan)
                 uint32_t c = (1u << L) - 1;
                 while (c < (1u << nt)) {
                     uint64_t low = 0;
                     for (int j = 0; j < nt; ++j)
                         if ((c >> j) & 1) low |= 1ull << tqs[j];
-                    const double sc = score_of(low);
-                    cands.push_back({sc, low});
-                    if (sc > best) { best = sc; bestmask = low; }
+                    cands.push_back({0.0, low});
                     const uint32_t u = c & (0u - c), w = c + u;
                     c = w | (((w ^ c) >> 2) / u);
                 }
+                const int nc = (int)cands.size();
+                // (sequential inside a rollout, which already runs on its own thread)
+                const int nthr = o.no_rollout ? 1
+                                              : std::max(1, std::min<int>(nc / 16, (int)std::thread::hardware_concurrency()));
+                if (nthr == 1) {
+                    for (int i = 0; i < nc; ++i) cands[i].first = score_of(cands[i].second);
+                } else {
+                    std::vector<std::thread> pool;
+                    for (int w = 0; w < nthr; ++w)
+                        pool.emplace_back([&, w]() {
+                            for (int i = w; i < nc; i += nthr) cands[i].first = score_of(cands[i].second);
+                        });
+                    for (auto& th : pool) th.join();
+                }
+                for (const auto& cd2 : cands)
+                    if (cd2.first > best) { best = cd2.first; bestmask = cd2.second; }
             }
             // physical position -> position after this pass for a given bottom set
             auto perm_for = [&](uint64_t mask, std::vector<int>& ls) {
@@ -1178,7 +1195,12 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                 size_t best_passes = SIZE_MAX;
                 double best_model = 1e300;
                 const bool tie_model = rollout_balance(dbl);
-                for (int k = 0; k < K && k < (int)cands.size(); ++k) {
+                // the K rollouts are independent greedy plans: run them on host threads, then
+                // pick in candidate order (the same choice as a sequential loop)
+                const int KK = std::min(K, (int)cands.size());
+                std::vector<size_t> np(KK, SIZE_MAX);
+                std::vector<double> mdl(KK, 0.0);
+                auto rollout = [&](int k) {
                     std::vector<int> ls;
                     const std::vector<int> pm = perm_for(cands[k].second, ls);
                     Context c2 = ctx;
@@ -1187,7 +1209,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                     Schedule s2;
                     std::vector<LOp> ops2;
                     std::string e2;
-                    if (build_schedule(ops2, c2, o2, s2, e2, &sub) != SV_OK) continue;
+                    if (build_schedule(ops2, c2, o2, s2, e2, &sub) != SV_OK) return;
                     // ties on the pass count: the modelled time sum_p max(cost_p, H) (H ~ 87 op-cost
                     // units per HBM pass) when SV_ROLLOUT_BALANCE, else the 1-step score
                     double model = 0;
@@ -1199,10 +1221,21 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                                     for (const LOp& op : st.ops) c += op_cost(op);
                             model += std::max(c, 87.0);
                         }
-                    if (s2.passes.size() < best_passes ||
-                        (tie_model && s2.passes.size() == best_passes && model < best_model - 1e-9)) {
-                        best_passes = s2.passes.size();
-                        best_model = model;
+                    np[k] = s2.passes.size();
+                    mdl[k] = model;
+                };
+                const int nthr = std::max(1, std::min<int>(KK, (int)std::thread::hardware_concurrency()));
+                std::vector<std::thread> pool;
+                for (int w = 0; w < nthr; ++w)
+                    pool.emplace_back([&, w]() {
+                        for (int k = w; k < KK; k += nthr) rollout(k);
+                    });
+                for (auto& th : pool) th.join();
+                for (int k = 0; k < KK; ++k) {
+                    if (np[k] == SIZE_MAX) continue;
+                    if (np[k] < best_passes || (tie_model && np[k] == best_passes && mdl[k] < best_model - 1e-9)) {
+                        best_passes = np[k];
+                        best_model = mdl[k];
                         bestmask = cands[k].second;
                     }
                 }
