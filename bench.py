@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-also", action="store_true", help="skip the c128 / multiplier sub-lines")
+    ap.add_argument("--control", default="nccl", choices=["nccl", "host"],
+                    help="sharded control plane (host: torch.distributed/gloo + CUDA IPC; ranks may share a GPU)")
     ap.add_argument("--no-e2e-cold", action="store_true")
     ap.add_argument("--e2e-cold-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
@@ -395,7 +397,7 @@ def time_case(P, torch, sv, c, text, dtype, workload, steps, warmup, world, loca
     info = plan.info()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    clk = ClockSampler(local)
+    clk = ClockSampler(torch.cuda.current_device())
     clk.start()
     clk.wait_running()
     barrier()
@@ -555,16 +557,22 @@ def run_ours(args):
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
-    torch.cuda.set_device(local)
+    # --control host: torch.distributed over gloo is the library's control plane and the
+    # exchanges go through CUDA IPC peer memory, so several ranks may share a GPU (used to
+    # exercise this N > 1 path on a one-GPU box; the driver's multi-GPU runs use NCCL)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.control == "host":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if world > 1 and args.workload == "supremacy" and args.qubits == 30:
         args.workload = "supremacy36"  # BASELINE config 5 is the N > 1 workload
     c, text, name = make_workload(args, world)
     n = c.n
     G = len(c.gates)
     if world > 1:
-        sv = P.StateVector.sharded(n, args.dtype)
+        sv = P.StateVector.sharded(n, args.dtype, control=args.control)
     else:
         sv = P.StateVector(n, args.dtype)
 

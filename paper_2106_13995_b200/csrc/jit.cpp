@@ -170,11 +170,23 @@ bool sign_xor() {
     return b;
 }
 
+// FFMA2 with a register multiplier issues once per 3 cycles on the FMA pipe, two scalar
+// FFMAs once per cycle each (profiles/r01_fp_rate.txt): SV_RT_SCALAR=1 emits the run-time
+// sign terms as two scalar FFMAs (F1) -- one more instruction, one FMA-pipe cycle less
+bool rt_scalar() {
+    static const bool b = [] {
+        const char* e = getenv("SV_RT_SCALAR");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
 std::string f2_term_rt(Em& e, const std::string& acc, const std::string& v, const cd& c, const std::string& r) {
     if (r.empty()) return f2_term(acc, v, c);
     const double cr = c.real(), ci = c.imag();
+    const char* FF = (!e.dbl && rt_scalar()) ? "F1(" : "F(";
     auto fm = [&](const std::string& u, const std::string& k) {
-        return acc.empty() ? "M(" + u + "," + k + ")" : "F(" + u + "," + k + "," + acc + ")";
+        return acc.empty() ? "M(" + u + "," + k + ")" : FF + u + "," + k + "," + acc + ")";
     };
     // a term with a run-time sign (+-1 per thread): flip the sign bits with an integer XOR
     // (ALU pipe) and keep the compile-time coefficient as an immediate / operand modifier
@@ -187,8 +199,8 @@ std::string f2_term_rt(Em& e, const std::string& acc, const std::string& v, cons
     if (ci == 0.0) return fm(v, rt_const(e, cr, r));
     if (cr == 0.0) return fm("I(" + v + ")", rt_const(e, ci, r));
     const std::string kr = rt_const(e, cr, r), ki = rt_const(e, ci, r);
-    const std::string inner = acc.empty() ? "M(" + v + "," + kr + ")" : "F(" + v + "," + kr + "," + acc + ")";
-    return "F(I(" + v + ")," + ki + "," + inner + ")";
+    const std::string inner = acc.empty() ? "M(" + v + "," + kr + ")" : FF + v + "," + kr + "," + acc + ")";
+    return FF + std::string("I(") + v + ")," + ki + "," + inner + ")";
 }
 
 // Pending per-qubit diagonal factors diag(s0, s1) not yet multiplied into the registers

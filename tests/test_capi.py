@@ -73,3 +73,20 @@ def test_plan_compile_parse_errors():
     assert lib.sv_plan_compile(b"qubits: 2\nH 0\n", 1, ctypes.byref(o), ctypes.byref(h)) == 1  # SV_ERR_ARG
     p = P.Plan("qubits: 4\nH 0; CNOT 0,1\nU 2 : 1,0,0,0,0,0,1,0\n")
     assert p.info()["gates"] == 3 and p.info()["n"] == 4
+
+
+def test_sharded_ex_argument_errors_before_any_cuda_call():
+    """sv_create_sharded_ex validates its arguments before touching CUDA or NCCL."""
+    from paper_2106_13995_b200._lib import Control, lib
+    h = ctypes.c_void_p()
+    # neither a unique id nor a control plane
+    assert lib.sv_create_sharded_ex(10, 1, None, None, 2, 0, None, None, ctypes.byref(h)) == 1
+    assert b"exactly one" in lib.sv_last_error()
+    # a control plane without callbacks
+    c = Control()
+    assert lib.sv_create_sharded_ex(10, 1, None, ctypes.byref(c), 2, 0, None, None, ctypes.byref(h)) == 1
+    # world not a power of two / too large, rank out of range
+    uid = (ctypes.c_uint8 * 128)()
+    for world, rank in ((3, 0), (16, 0), (2, 2)):
+        assert lib.sv_create_sharded_ex(10, 1, ctypes.cast(uid, ctypes.c_void_p), None, world, rank, None, None,
+                                        ctypes.byref(h)) == 1

@@ -209,3 +209,26 @@ def test_ipc_ranks_with_different_plans_fail_before_launch():
     for r in res:
         assert r["status"] == 7, r  # SV_ERR_STATE
         assert "differs between ranks" in r["msg"]
+
+
+def test_bench_multirank_host_control_plane():
+    """bench.py's N > 1 path (torchrun, one process per rank, sharded state, max over ranks,
+    one JSON line from rank 0) with two ranks sharing this GPU through the host control plane
+    (--control host): weak scaling, 2^24 amplitudes per rank."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--control", "host", "--workload", "weak", "--qubits", "24", "--steps", "3",
+           "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["n_qubits"] == 25 and d["value"] > 0
+    assert d["config"]["swaps_per_step"] >= 1 and d["scaling"] == "weak"
+    assert d["e2e"]["value"] > 0

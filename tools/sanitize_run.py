@@ -74,3 +74,43 @@ for dt, tol in (("c64", 1e-5), ("c128", 1e-12)):
         sv.apply_circuit(t)
         check(sv.amplitudes(), oracle.simulate(t, np.full(1 << 16, 2.0 ** -8, complex)), tol)
 print("sanitize run ok")
+
+# Round-2 additions: borrowed buffer canonicalised after a relabelling plan (sv_wrap),
+# sv_device_ptr canonicalisation, dense-k with many controls (bit-insertion table), and the
+# pass-pair kernels (SV_PAIR=1 is read once per process: enabled here through the env var
+# set by the caller, else skipped).
+import torch  # noqa: E402
+
+c = W.supremacy(4, 4, 10, seed=3)
+t = W.to_text(c)
+ref = oracle.simulate(t)
+for dt, tol in (("c64", 1e-5), ("c128", 1e-12)):
+    buf = torch.zeros(1 << 16, dtype=torch.complex64 if dt == "c64" else torch.complex128, device="cuda")
+    buf[0] = 1
+    with P.StateVector.wrap(buf, 16) as sv:
+        sv.apply_circuit(t)
+        sv.sync()
+        check(buf.cpu().numpy(), ref, tol)
+    with P.StateVector(16, dt) as sv:
+        sv.apply_circuit(t)
+        sv.device_ptr()
+        check(sv.amplitudes(), ref, tol)
+n = 16
+psi0 = W.random_state(n, 5)
+X = np.array([[0, 1], [1, 0]], complex)
+ctl = list(range(1, 15))
+want = psi0.copy()
+idx = np.flatnonzero([all((i >> q) & 1 for q in ctl) for i in range(1 << n)])
+want[idx] = oracle.apply_gate(np.ascontiguousarray(psi0[idx]), X, [0])
+with P.StateVector(n, "c128") as sv:
+    sv.set_amplitudes(psi0)
+    sv.apply_gate(X, [0], ctl)
+    check(sv.amplitudes(), want, 1e-14)
+if os.environ.get("SV_PAIR") == "1":
+    c = W.supremacy(5, 4, 14, seed=2)
+    t = W.to_text(c)
+    ref = oracle.simulate(t)
+    with P.StateVector(20, "c64") as sv:
+        sv.apply_circuit(t)
+        check(sv.amplitudes(), ref, 1e-5)
+print("sanitize run (round-2 paths) ok")
