@@ -800,12 +800,17 @@ int tiles_per_cta() {
 // CTAs per SM the register allocation must allow (SV_MIN_WARPS: resident warps per SM).
 // Measured (profiles/r01_min_warps.txt, 30 q supremacy): c64 24.85 ms at 16 warps, 24.2 at
 // 20, 27.6 at 24; c128 no better than noise at 20, 62 ms at 24 -- 20 (c64) / 16 (c128).
-int min_blocks(int threads, bool dbl) {
+int min_blocks(int threads, bool dbl, bool heavy = false) {
     static const int w = [] {
         const char* e = getenv("SV_MIN_WARPS");
         return e ? atoi(e) : 0;
     }();
-    const int warps = w > 0 ? w : dbl ? 16 : 20;
+    // heavy passes (one register bit fewer, twice the threads per tile): SV_MIN_WARPS_HEAVY
+    static const int wh = [] {
+        const char* e = getenv("SV_MIN_WARPS_HEAVY");
+        return e ? atoi(e) : 0;
+    }();
+    const int warps = (heavy && wh > 0) ? wh : w > 0 ? w : dbl ? 16 : 20;
     return std::max(1, std::min(32, warps * 32 / threads));
 }
 
@@ -913,7 +918,9 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     } else {
     if (xS >= 0) o << "struct XT { C* p[8]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ","
-      << (pf ? std::max(1, min_blocks(threads, sym.dbl) / 2) : min_blocks(threads, sym.dbl)) << ") svpass(C* __restrict__ psi"
+      << (pf ? std::max(1, min_blocks(threads, sym.dbl) / 2)
+             : min_blocks(threads, sym.dbl, rb < (sym.dbl ? 4 : 5)))
+      << ") svpass(C* __restrict__ psi"
       << (basis_in ? ",unsigned long long kb" : "") << (uniform_in ? ",const C u0" : "")
       << (xS >= 0 ? ",const XT xo,unsigned xr" : "") << "){\n";
     if (pf) o << "extern __shared__ C sm[];\n";

@@ -1242,7 +1242,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
             }
             perm = perm_for(bestmask, lowset);
         }
-        if (getenv("SV_PLAN_DEBUG")) {
+        if (getenv("SV_PLAN_DEBUG") && !o.no_rollout) {
             fprintf(stderr, "pass %zu: ops %zu deferred %zu S=", out.passes.size(), pass_ops.size(), next.size());
             for (int q = 0; q < 64; ++q) if ((S >> q) & 1) fprintf(stderr, "%d ", q);
             fprintf(stderr, "| low ->");

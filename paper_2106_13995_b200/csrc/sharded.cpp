@@ -243,6 +243,10 @@ sv_status run_ops(sv_state_s* s, std::vector<std::vector<LOp>>& ops, const RunOp
 // Exchange the g global bits with the g top local bits (whole-block all-to-all, N1/N2).
 sv_status exchange_all(sv_state_s* s, sv_run_stats* st, std::string& err) {
     const int g = s->g, P = s->world;
+    if (!s->virt && !s->comm) {
+        err = "no NCCL transport (host control plane) and the peer-memory exchange is unavailable";
+        return SV_ERR_STATE;
+    }
     const size_t chunk = (size_t)(s->local_amps() >> g) * s->amp_bytes();
     if (s->virt) {
         for (int r = 0; r < P; ++r)
@@ -322,6 +326,10 @@ sv_status exchange_one(sv_state_s* s, int j, std::string& err) {
         const sv_status r = peer_flip(s, nullptr, err);
         if (r != SV_OK) return r;
     } else {
+        if (!s->comm) {
+            err = "no NCCL transport (host control plane) and the peer-memory exchange is unavailable";
+            return SV_ERR_STATE;
+        }
         const int b = (s->rank >> j) & 1;
         const int peer = s->rank ^ (1 << j);
         char* mine = (char*)s->d + (b ? 0 : half);
