@@ -677,6 +677,14 @@ def run_ours(args):
                     "includes": "IR text through sv_apply_circuit (plan cache warm) + init + passes + 20-qubit marginal D2H"},
             "e2e_cold": cold,
             "also": also or None,
+            # north_star: the paper's own speedups, quoted with its hardware, as context only
+            "paper_context": {
+                "supremacy": "CuPy ~2x faster than C++ simulators (QSim via Cirq), up to 28 q (P:24, P:123)",
+                "multiplier": "CuPy almost 22x faster than C++-based simulators, 13-28 q (P:24)",
+                "hardware": "Google Colab Tesla T4 16 GB on PCIe, CUDA 11.2, Xeon 2.2 GHz, 12 GB RAM (P:69); "
+                            "no absolute times published (figures elided)",
+                "this_run_vs_oracle": (res["value"] / cpu["value"]) if (cpu and cpu.get("value")) else None,
+            },
             "gpu_launches": int(args.steps * launches),
             "clocks": res["clocks"],
             "wall_s_timed_region": res["wall"],
