@@ -220,6 +220,27 @@ class StateVector:
         check(lib.sv_amplitudes(self._h, int(first), int(count), out.ctypes.data_as(ctypes.c_void_p)))
         return out
 
+    def gather_amplitudes(self, root: int = 0, group=None) -> Optional[np.ndarray]:
+        """Sharded states (collective): every rank reads the part of the logical index range it
+        holds and `root` receives the whole 2^n vector (small n only); other
+        ranks get None.  Unsharded states: all amplitudes."""
+        if self.world == 1:
+            return self.amplitudes()
+        import torch
+        import torch.distributed as dist
+        L = 1 << self.n_local
+        mine = self.amplitudes(self.rank * L, L)
+        t = torch.from_numpy(mine.view(np.float64 if self.dtype == SV_C128 else np.float32).copy())
+        backend_cuda = dist.get_backend(group) == "nccl"
+        if backend_cuda:
+            t = t.cuda()
+        parts = [torch.empty_like(t) for _ in range(self.world)] if dist.get_rank(group) == root else None
+        dist.gather(t, parts, dst=root, group=group)
+        if parts is None:
+            return None
+        flat = torch.cat([p.cpu() for p in parts]).numpy()
+        return flat.view(_NP[self.dtype])
+
     def probabilities(self, qubits: Iterable[int]) -> np.ndarray:
         qs = list(qubits)
         q = (ctypes.c_int * max(1, len(qs)))(*qs)

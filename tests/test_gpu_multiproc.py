@@ -190,6 +190,21 @@ def test_ipc_borrowed_shard_buffer_holds_logical_order():
     assert_close(gather(res), oracle.simulate(text), "c128", W.gate_count(c))
 
 
+def _job_gather(P, rank, world, text=None, n=None):
+    with P.StateVector.sharded(n, "c128", control="host") as sv:
+        sv.apply_circuit(text)
+        full = sv.gather_amplitudes(root=0)
+        return {"full": full}
+
+
+def test_ipc_gather_amplitudes_to_rank0():
+    c = W.supremacy(4, 4, 8, seed=4)
+    text = W.to_text(c)
+    res = run_ranks(4, Job(_job_gather, text=text, n=16))
+    assert res[0]["full"] is not None and all(r["full"] is None for r in res[1:])
+    assert_close(res[0]["full"], oracle.simulate(text), "c128", W.gate_count(c))
+
+
 def _job_mismatch(P, rank, world, texts=None):
     from paper_2106_13995_b200._lib import SvError
     with P.StateVector.sharded(12, "c128", control="host") as sv:
