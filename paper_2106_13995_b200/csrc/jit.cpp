@@ -814,6 +814,16 @@ int min_blocks(int threads, bool dbl, bool heavy = false) {
     return std::max(1, std::min(32, warps * 32 / threads));
 }
 
+// SV_STREAM_HINTS=1: pass loads / stores with the streaming cache hints (ld.global.cs /
+// st.global.cs, evict-first): each amplitude is touched once per pass
+bool stream_hints() {
+    static const bool b = [] {
+        const char* e = getenv("SV_STREAM_HINTS");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
 // run-length emission of  sum_i ((t >> i) & 1) << dst[i]
 std::string deposit_expr(const std::vector<int>& dst, bool wide) {
     std::string ex;
@@ -890,6 +900,15 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         // FFMA2 issues at 1/3 per cycle on B200, two scalar FFMAs at 1 each
         // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes
         o << (scalar_fma() ? "#define F F1\n" : "#define F F2\n");
+    }
+    if (md.prelude && stream_hints()) {
+        // streaming cache hints: every amplitude is read once and written once per pass
+        if (sym.dbl)
+            o << "__device__ __forceinline__ C LDS_(const C* p){const double2 d=__ldcs((const double2*)p);return mk(d.x,d.y);}\n"
+                 "__device__ __forceinline__ void STS_(C* p,C v){__stcs((double2*)p,make_double2(v.x,v.y));}\n";
+        else
+            o << "#define LDS_(p) __ldcs((const unsigned long long*)(p))\n"
+                 "#define STS_(p,v) __stcs((unsigned long long*)(p),(v))\n";
     }
     if (md.prelude && md.ldcg) {
         // loads of a paired pass go to L2 only (ld.global.cg): the second pass of a pair reads
@@ -1127,7 +1146,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             o << "\n";
         } else if (!reads_smem) {
             for (int s = 0; s < R; ++s)
-                o << reg(s) << (md.ldcg ? "=LDG(psi+g+" : "=psi[g+") << goff[s] << (md.ldcg ? "ull);" : "ull];");
+                o << reg(s) << (md.ldcg ? "=LDG(psi+g+" : stream_hints() ? "=LDS_(psi+g+" : "=psi[g+") << goff[s]
+                  << ((md.ldcg || stream_hints()) ? "ull);" : "ull];");
             o << "\n";
         } else {
             if (si > first) o << "__syncthreads();\n";
@@ -1224,7 +1244,10 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                 }
             }
             if (xS < 0) {
-                for (int s = 0; s < R; ++s) o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
+                for (int s = 0; s < R; ++s) {
+                    if (stream_hints()) o << "STS_(psi+g+" << goff[s] << "ull," << reg(s) << ");";
+                    else o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
+                }
             } else {
                 // store bits above xS-1 select the destination rank; when no tile qubit lands
                 // there the whole tile goes to one peer (its rank = the tile base's top bits)
