@@ -152,6 +152,9 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
     for (const PassPlan& pp : sc.passes) {
         ++pi;
         cudaError_t e;
+        SvRange nv_(SvRange::enabled() ? "sv pass " + std::to_string(pi - 1) +
+                                             (pp.kind == PassPlan::PERM ? " (gather)" : pp.kind == PassPlan::DENSE ? " (dense-k)" : "")
+                                       : std::string());
         if (pp.paired_second) {
             // ran inside the previous pass's pair kernel
             if (ev) CK(cudaEventRecord((*ev)[pi], s->stream));
@@ -672,6 +675,7 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
         if (st != SV_OK) return st;
     }
     if (!p->jitted && p->opts.use_jit()) {
+        SvRange nv_("sv jit (NVRTC)");
         const sv_status st = jit_prepare(p->sched, err, true);
         if (st != SV_OK) return fail(st, err);
         p->jitted = true;
@@ -760,6 +764,7 @@ sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* o
     if (opts) o = *opts;
     key.append(reinterpret_cast<const char*>(&o), sizeof(o));
     key.append(ir_text);
+    SvRange nv_("sv_apply_circuit");
     PlanRef p;
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -773,7 +778,10 @@ sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* o
     sv_status st = SV_OK;
     if (!p) {
         sv_plan raw = nullptr;
-        st = sv_plan_compile(ir_text, s->dtype, opts, &raw);
+        {
+            SvRange nv2_("sv_plan_compile");
+            st = sv_plan_compile(ir_text, s->dtype, opts, &raw);
+        }
         if (st != SV_OK) return st;
         p = PlanRef(raw, [](sv_plan_s* q) { sv_plan_destroy(q); });
         std::lock_guard<std::mutex> lk(mu);
@@ -811,6 +819,7 @@ sv_status sv_amplitudes(sv_state s, uint64_t first, uint64_t count, void* host_o
 
 sv_status sv_probabilities(sv_state s, const int* qubits, int nq, double* host_out) {
     if (!s || !host_out || (nq > 0 && !qubits)) return fail(SV_ERR_ARG, "NULL argument");
+    SvRange nv_("sv_probabilities");
     if (nq < 0 || nq > s->n || nq > 28) return fail(SV_ERR_RANGE, "nq must be in [0, min(n, 28)]");
     {
         const sv_status st = materialize(s);

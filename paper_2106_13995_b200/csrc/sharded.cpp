@@ -473,6 +473,7 @@ sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
         ShardStep& step = sp->steps[si];
         sv_status r;
         if (step.exchange) {
+            SvRange nv_(peer ? "sv exchange (peer flip)" : "sv exchange (NCCL)");
             r = peer ? peer_flip(s, stats, err) : exchange_all(s, stats, err);
         } else {
             const bool feeds = peer && si + 1 < sp->steps.size() && sp->steps[si + 1].exchange;

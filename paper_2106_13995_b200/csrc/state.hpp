@@ -8,8 +8,31 @@
 
 #include "engine.hpp"
 
+#include <cstdlib>
+
+#include <nvtx3/nvToolsExt.h>
+
 // sets the thread-local sv_last_error() message and returns st (capi.cpp)
 sv_status svb_fail(sv_status st, const std::string& msg);
+
+// NVTX ranges around the library's phases (plan, each pass launch, exchanges, readouts) when
+// SV_NVTX=1, for timelines and ncu --nvtx filters; nothing otherwise.
+struct SvRange {
+    bool on;
+    explicit SvRange(const std::string& name) : on(enabled()) {
+        if (on) nvtxRangePushA(name.c_str());
+    }
+    ~SvRange() {
+        if (on) nvtxRangePop();
+    }
+    static bool enabled() {
+        static const bool b = [] {
+            const char* e = getenv("SV_NVTX");
+            return e && atoi(e) != 0;
+        }();
+        return b;
+    }
+};
 
 struct sv_state_s {
     int n = 0;              // logical qubits
