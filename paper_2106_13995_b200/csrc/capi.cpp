@@ -124,6 +124,7 @@ void free_state(sv_state_s* s) {
     if (s->d_gather) cudaFree(s->d_gather);
     if (s->d_scratch) cudaFree(s->d_scratch);
     if (s->pair_ctl) cudaFree(s->pair_ctl);
+    if (s->small_bar) cudaFree(s->small_bar);
     if (s->xbuf) cudaFree(s->xbuf);
     if (s->comm) comm_destroy(s->comm);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
@@ -148,6 +149,29 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
         }
         CK(cudaEventRecord((*ev)[0], s->stream));
     }
+    if (sc.small_fn[0]) {
+        // small state: the whole schedule in one kernel (grid barrier between passes)
+        if (!s->small_bar) {
+            CK(cudaMalloc(&s->small_bar, 16));
+            CK(cudaMemsetAsync(s->small_bar, 0, 16, s->stream));
+        }
+        const int variant = basis >= 0 ? 1 : uniform ? 2 : 0;
+        const cudaError_t e = jit_launch_small(sc, psi, s->small_bar, variant, basis >= 0 ? (uint64_t)basis : 0,
+                                               uniform_amp(s->n), s->dbl, s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "small-state schedule launch");
+        if (ev)
+            for (size_t i = 1; i <= sc.passes.size(); ++i) CK(cudaEventRecord((*ev)[i], s->stream));
+        if (st) {
+            st->passes += sc.passes.size();
+            st->launches += 1;
+            for (const PassPlan& pp : sc.passes) {
+                st->stages += pp.nstages;
+                st->hbm_bytes += 2ull * pp.touched_amps * s->amp_bytes();
+            }
+            if (variant) st->hbm_bytes -= sc.passes[0].touched_amps * s->amp_bytes();
+        }
+        return SV_OK;
+    }
     size_t pi = 0;
     for (const PassPlan& pp : sc.passes) {
         ++pi;
@@ -165,6 +189,7 @@ sv_status run_schedule(sv_state_s* s, void* psi, const Schedule& sc, sv_run_stat
             const size_t need = (size_t)(pp.pair_chunks + 1) * 8;
             if (s->pair_ctl_bytes < need) {
                 if (s->pair_ctl) cudaFree(s->pair_ctl);
+    if (s->small_bar) cudaFree(s->small_bar);
                 s->pair_ctl = nullptr;
                 s->pair_ctl_bytes = 0;
                 CK(cudaMalloc(&s->pair_ctl, need));
@@ -683,10 +708,10 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
     // fused init: a deferred basis state is synthesised by the first pass instead of written
     int64_t kb = -1;
     bool unif = false;
-    const bool basis_variant = !p->sched.passes.empty() &&
-                               (p->sched.passes[0].jit_fn_basis || p->sched.passes[0].pair_fn_basis);
-    const bool unif_variant = !p->sched.passes.empty() &&
-                              (p->sched.passes[0].jit_fn_unif || p->sched.passes[0].pair_fn_unif);
+    const bool basis_variant = !p->sched.passes.empty() && (p->sched.passes[0].jit_fn_basis ||
+                                                            p->sched.passes[0].pair_fn_basis || p->sched.small_fn[1]);
+    const bool unif_variant = !p->sched.passes.empty() && (p->sched.passes[0].jit_fn_unif ||
+                                                           p->sched.passes[0].pair_fn_unif || p->sched.small_fn[2]);
     if (s->lazy_basis >= 0 && !p->opts.use_graph && basis_variant) {
         kb = s->lazy_basis;
         s->lazy_basis = -1;  // the map is the identity after an init
@@ -697,6 +722,10 @@ sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
     }
     sv_status st = canonicalize(s);  // the plan assumes the identity layout
     if (st != SV_OK) return st;
+    if (p->sched.small_fn[0] && !s->small_bar) {  // before any graph capture: no allocation inside one
+        CK(cudaMalloc(&s->small_bar, 16));
+        CK(cudaMemsetAsync(s->small_bar, 0, 16, s->stream));
+    }
     if (p->opts.use_graph) {
         if (!p->graph || p->graph_ptr != s->d || p->graph_stream != s->stream) {
             if (p->graph) cudaGraphExecDestroy(p->graph);

@@ -153,6 +153,12 @@ struct PassPlan {
 struct Schedule {
     std::vector<PassPlan> passes;
     uint64_t stages = 0;
+    // small states (jit.cpp gen_small_source): the whole schedule as one kernel, per input
+    // variant (0 reads the state, 1 basis input, 2 uniform input); null = per-pass launches
+    void* small_fn[3] = {nullptr, nullptr, nullptr};
+    int small_threads = 0;
+    size_t small_smem = 0;
+    unsigned small_grid = 0;
     std::vector<int> end_phys;   // qubit map after the schedule if it changes the layout (else empty)
 };
 

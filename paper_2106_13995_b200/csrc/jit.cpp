@@ -1388,6 +1388,70 @@ std::string gen_pair_source(const PassPlan& A, const PassPlan& B, const PairGeom
     return src + o.str();
 }
 
+// ------------------------------------------------------------------ small states
+// A state of a few tiles (configs 1-2 latency regime: 12 q complex128 = 2 tiles of 2^11) runs
+// its whole single-GPU schedule in ONE kernel: every pass is a device function, the CTAs
+// (grid = the largest tile count, all resident) take the pass's tiles, then meet at a grid
+// barrier (one global counter, reset by the last CTA to leave) before the next pass reads
+// what other CTAs wrote (loads through L2, ld.global.cg).  One launch instead of one per
+// pass.
+bool small_fuse_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SMALL_FUSE");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
+std::string gen_small_source(const std::vector<const PassPlan*>& ps, int variant, int& threads, size_t& smem,
+                             unsigned& grid) {
+    std::string src;
+    smem = 16;
+    grid = 1;
+    threads = 0;
+    for (size_t i = 0; i < ps.size(); ++i) {
+        const PassPlan& pp = *ps[i];
+        GenMode md;
+        md.device_fn = true;
+        md.ldcg = true;
+        md.prelude = i == 0;
+        md.fname = "tile" + std::to_string(i);
+        int th, tpc;
+        size_t sm = 0;
+        bool pers;
+        cd out;
+        src += gen_pass_source(*pp.sym, pp.ntiles, th, sm, pers, tpc, i == 0 && variant == 1, -1, i == 0 && variant == 2,
+                               pp.carry_in, pp.carry_next ? &out : nullptr, &md);
+        threads = th;
+        smem = std::max(smem, sm);
+        grid = std::max<unsigned>(grid, (unsigned)pp.ntiles);
+    }
+    std::ostringstream o;
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ",1) svpass(C* __restrict__ psi,"
+      << "unsigned* __restrict__ bar" << (variant == 1 ? ",const unsigned long long kb" : "")
+      << (variant == 2 ? ",const C u0" : "") << "){\n";
+    o << "extern __shared__ C sm[];\n";
+    for (size_t i = 0; i < ps.size(); ++i) {
+        const PassPlan& pp = *ps[i];
+        if (i > 0) {
+            // grid barrier: every CTA's stores of the previous pass before anyone's loads
+            o << "__syncthreads();\nif(threadIdx.x==0){__threadfence();atomicAdd(bar,1u);unsigned v;for(;;){"
+                 "asm volatile(\"ld.acquire.gpu.global.u32 %0,[%1];\":\"=r\"(v):\"l\"(bar):\"memory\");if(v>="
+              << i << "u*gridDim.x)break;}__threadfence();}\n__syncthreads();\n";
+        }
+        o << "for(unsigned long long tl_=blockIdx.x;tl_<" << pp.ntiles << "ull;tl_+=gridDim.x){\n";
+        o << "unsigned long long base=tl_;\n";
+        for (int q : pp.sym->tq)
+            o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
+        o << "tile" << i << "(psi,base,sm" << (i == 0 && variant == 1 ? ",kb" : "") << (i == 0 && variant == 2 ? ",u0" : "")
+          << ");\n__syncthreads();\n}\n";
+    }
+    // the last CTA to leave resets the counters for the next launch on this stream
+    o << "if(threadIdx.x==0){__threadfence();const unsigned x=atomicAdd(bar+1,1u);if(x==gridDim.x-1){"
+         "atomicExch(bar,0u);atomicExch(bar+1,0u);}}\n}\n";
+    return src + o.str();
+}
+
 // Measured on B200 (profiles/r02_pair.txt): slower than the two passes it replaces (30 q
 // c64 pairs (0,1) 8.3 vs 7.26 ms, (4,5) 6.9 vs 5.9 ms).  With blocks of about a wave the
 // second pass misses L2 entirely (DRAM bytes = two passes' worth); with blocks small enough
@@ -1602,6 +1666,35 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
         std::string err;
     };
     std::vector<PairJob> pjobs;
+    // small states: the whole schedule in one kernel (three input variants)
+    if (with_basis && small_fuse_enabled() && !sc.passes.empty() && !sc.small_fn[0]) {
+        bool ok = sc.passes.size() >= 2;
+        int th0 = -1;
+        std::vector<const PassPlan*> ps;
+        for (const PassPlan& pp : sc.passes) {
+            ok &= pp.kind == PassPlan::TILE && pp.sym && pp.xS < 0 && pp.ntiles > 0 && pp.ntiles <= 64;
+            if (!ok) break;
+            const int th = 1 << ((int)pp.sym->tq.size() - pp.sym->rb);
+            ok &= th0 < 0 || th == th0;
+            th0 = th;
+            ps.push_back(&pp);
+        }
+        if (ok) {
+            jit_carries(sc);
+            for (int v = 0; v < 3; ++v) {
+                int threads;
+                size_t smem;
+                unsigned grid;
+                const std::string src = gen_small_source(ps, v, threads, smem, grid);
+                const sv_status r = jit_compile(src, smem, &sc.small_fn[v], err);
+                if (r != SV_OK) return r;
+                sc.small_threads = threads;
+                sc.small_smem = smem;
+                sc.small_grid = grid;
+            }
+            return SV_OK;  // the per-pass kernels are not needed
+        }
+    }
     if (with_basis && pair_enabled()) {
         jit_carries(sc);
         for (size_t i = 0; i + 1 < sc.passes.size(); ++i) {
@@ -1800,6 +1893,23 @@ cudaError_t jit_launch_pair(const PassPlan& pp, void* psi, void* ctl, int varian
     void* args3[] = {&psi, &ctl, &D, &LK, pp.sym->dbl ? (void*)&u2 : (void*)&u1};
     void** args = variant == 1 ? args2 : variant == 2 ? args3 : args1;
     return cudaLaunchKernel(fn, dim3(pp.pair_grid), dim3((unsigned)pp.pair_threads), args, pp.pair_smem, stream);
+}
+
+cudaError_t jit_launch_small(const Schedule& sc, void* psi, void* bar, int variant, uint64_t kb, double amp,
+                             bool dbl, cudaStream_t stream) {
+    unsigned long long k = kb;
+    struct alignas(16) C2 {
+        double x, y;
+    } u2{amp, 0.0};
+    unsigned long long u1;
+    const float f[2] = {(float)amp, 0.0f};
+    std::memcpy(&u1, f, 8);
+    void* args1[] = {&psi, &bar};
+    void* args2[] = {&psi, &bar, &k};
+    void* args3[] = {&psi, &bar, dbl ? (void*)&u2 : (void*)&u1};
+    void** args = variant == 1 ? args2 : variant == 2 ? args3 : args1;
+    return cudaLaunchKernel(sc.small_fn[variant], dim3(sc.small_grid), dim3((unsigned)sc.small_threads), args,
+                            sc.small_smem, stream);
 }
 
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream) {

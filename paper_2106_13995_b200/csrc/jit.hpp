@@ -37,6 +37,10 @@ cudaError_t jit_launch_x(const PassPlan& pp, void* psi, void* const outs[8], uns
 // variant 0 = reads psi, 1 = basis-state input kb, 2 = uniform input amp
 cudaError_t jit_launch_pair(const PassPlan& pp, void* psi, void* ctl, int variant, uint64_t kb, double amp,
                             cudaStream_t stream);
+// small-state schedule in one kernel (sc.small_fn[variant]); bar = two zeroed device words
+// (left zeroed by the kernel); variant 0 = reads psi, 1 = basis input kb, 2 = uniform input amp
+cudaError_t jit_launch_small(const Schedule& sc, void* psi, void* bar, int variant, uint64_t kb, double amp,
+                             bool dbl, cudaStream_t stream);
 // whole-permutation pass (out-of-place gather)
 std::string gen_perm_source(const PassPlan& pp, bool dbl, int& threads);
 cudaError_t jit_launch_perm(const PassPlan& pp, const void* in, void* out, cudaStream_t stream);

@@ -69,6 +69,7 @@ struct sv_state_s {
     double* d_scratch = nullptr;
     size_t scratch_doubles = 0;
     void* pair_ctl = nullptr;     // work ticket + chunk counters of pass-pair kernels
+    void* small_bar = nullptr;    // grid-barrier counters of small-state schedules (kept zero between launches)
     size_t pair_ctl_bytes = 0;
     int device = 0;
     // Deferred basis-state initialisation (single GPU): the state is |lazy_basis> but not yet

@@ -43,6 +43,13 @@ def gpu_us(sv, plan, init, reps=REPS):
 rows = []
 c1 = W.supremacy(4, 3, 10, seed=0)
 t1 = W.to_text(c1)
+for extra in ((4, 4, 10, 16),):  # a 16 q circuit too (3 passes in complex128)
+    ce = W.supremacy(extra[0], extra[1], extra[2], seed=0)
+    plan = P.Plan(W.to_text(ce), "c128")
+    with P.StateVector(extra[3], "c128") as sv:
+        dev_us, wall_us = gpu_us(sv, plan, sv.init_zero)
+    rows.append({"config": "16q supremacy d10 c128", "gates": W.gate_count(ce), "passes": plan.info()["passes"],
+                 "device_us": dev_us, "wall_us": wall_us})
 for graph in (False, True):
     plan = P.Plan(t1, "c128", use_graph=graph)
     with P.StateVector(12, "c128") as sv:
