@@ -824,6 +824,14 @@ bool stream_hints() {
     return b;
 }
 
+int l2_prefetch() {
+    static const int d = [] {
+        const char* e = getenv("SV_L2PF");
+        return e ? atoi(e) : 0;
+    }();
+    return d;
+}
+
 // run-length emission of  sum_i ((t >> i) & 1) << dst[i]
 std::string deposit_expr(const std::vector<int>& dst, bool wide) {
     std::string ex;
@@ -997,6 +1005,22 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             const int q = sym.tq[b];
             o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
         }
+    // SV_L2PF = D > 0: L2 prefetch of the tile D tiles ahead (about the one a CTA of the next
+    // wave will load): one cp.async.bulk.prefetch.L2 per 256-byte run of the tile (its low
+    // qubits are physical 0..L-1), issued by the first 2^(m-L) threads
+    const int L2 = sym.dbl ? 4 : 5;
+    if (l2_prefetch() > 0 && !md.device_fn && !pf && tpc == 1 && !basis_in && !uniform_in && m > L2 &&
+        (1 << (m - L2)) <= tthreads) {
+        o << "{const unsigned long long nt_=(unsigned long long)blockIdx.x+" << l2_prefetch() << "ull;\n"
+          << "if(nt_<" << ntiles << "ull&&threadIdx.x<" << (1 << (m - L2)) << "u){unsigned long long nb_=nt_;\n";
+        for (int b = 0; b < m; ++b) {
+            const int q = sym.tq[b];
+            o << "nb_=((nb_>>" << q << ")<<" << (q + 1) << ")|(nb_&" << ((1ull << q) - 1) << "ull);";
+        }
+        std::vector<int> hi(sym.tq.begin() + L2, sym.tq.end());
+        o << "\nconst unsigned t=threadIdx.x;nb_|=" << deposit_expr(hi, true) << ";\n"
+          << "asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], 256;\"::\"l\"(psi+nb_):\"memory\");}}\n";
+    }
     const std::string SM = pf ? "bc" : "sm";
     PassState ps;
     ps.fac = carry_in;  // global phase left pending by the previous pass of the schedule
