@@ -114,3 +114,18 @@ if os.environ.get("SV_PAIR") == "1":
         sv.apply_circuit(t)
         check(sv.amplitudes(), ref, 1e-5)
 print("sanitize run (round-2 paths) ok")
+
+# small-state schedule in one kernel (grid barrier between passes), all input variants
+c = W.supremacy(4, 3, 10, seed=0)
+t = W.to_text(c)
+ref = oracle.simulate(t)
+for dt, tol in (("c64", 1e-5), ("c128", 1e-12)):
+    with P.StateVector(12, dt) as sv:
+        for _ in range(3):
+            sv.init_zero()
+            sv.apply_circuit(t)
+            check(sv.amplitudes(), ref, tol)
+        sv.init_uniform()
+        sv.apply_circuit(t)
+        check(sv.amplitudes(), oracle.simulate(t, np.full(1 << 12, 2.0 ** -6, complex)), tol)
+print("sanitize run (small-state schedule) ok")
