@@ -564,11 +564,11 @@ sv_status sv_apply_gate(sv_state s, const double* mat, int k, const int* targets
     plan.lcirc = plan.circ;
     plan.dtype = s->dtype;
     plan.opts.fuse = false;
-    // k <= 3: the specialised dense-k kernel (registers, two groups in flight per thread,
-    // controlled subset only) beats the single-stage interpreter pass for every gate kind and
-    // target position (profiles/r01_per_gate.txt: 30 q c64 78-84 % of the HBM peak on full
-    // passes vs 42-76 %); wider gates keep the interpreter
-    if (k <= 3) plan.opts.force_kernel = SV_KERNEL_DENSE;
+    // every k: the specialised dense-k kernels (registers, controlled subset only) beat the
+    // single-stage interpreter pass (profiles/r01_per_gate.txt: 30 q c64 78-84 % of the HBM
+    // peak on full passes vs 42-76 % for k <= 3; profiles/r02_dense_wide.txt: k = 4 / 5 with
+    // one group per thread 13.9 -> 3.3 ms and 34.5 -> 5.9 ms at 30 q c64)
+    plan.opts.force_kernel = SV_KERNEL_DENSE;
     return sv_plan_apply(s, &plan, nullptr);
 }
 

@@ -443,6 +443,46 @@ __global__ void __launch_bounds__(256) dense_kt_kernel(typename V2<real>::t* __r
     }
 }
 
+// Specialised dense-k for k = 4, 5 (sv_apply_gate of wide blocks): one group of 2^K amplitudes
+// per thread in registers, compile-time matrix indices (the entries are read from the kernel
+// parameters, a uniform constant-bank operand of each FFMA), scalar FMAs (4 per complex
+// multiply-add: the FP32 lane rate of FFMA with a register multiplier; FFMA2 would issue at
+// 2/3 of it).  FP-bound at k = 5: 8 * 2^k flops per amplitude.
+template <typename real, int K, int U>
+__global__ void __launch_bounds__(128) dense_kw_kernel(typename V2<real>::t* __restrict__ psi,
+                                                       const __grid_constant__ DenseParams<real> P,
+                                                       uint64_t groups) {
+    using V = typename V2<real>::t;
+    constexpr int D = 1 << K;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t base = g;
+        for (int j = 0; j < P.nsorted; ++j) {
+            const int q = P.sorted[j];
+            base = ((base >> q) << (q + 1)) | (base & ((1ull << q) - 1));
+        }
+        base |= P.cmask;
+        V x[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[c] = psi[base + P.off[c]];
+        // U rows per iteration: the inputs stay in registers, the matrix entries of a row are
+        // read per iteration (a fully unrolled row loop keeps too many values live: spills)
+#pragma unroll(U)
+        for (int r = 0; r < D; ++r) {
+            real ar = 0, ai = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const real mr = P.M[2 * (r * D + c)], mi = P.M[2 * (r * D + c) + 1];
+                ar = fma(x[c].x, mr, ar);
+                ar = fma(-x[c].y, mi, ar);
+                ai = fma(x[c].x, mi, ai);
+                ai = fma(x[c].y, mr, ai);
+            }
+            psi[base + P.off[r]] = mk<V>(ar, ai);
+        }
+    }
+}
+
 // complex64 dense-k with qubit 0 free (no gate qubit on it): groups 2h and 2h+1 have bases
 // b and b+1, so one 16-byte load fetches the same matrix index of both groups; two such
 // group pairs in flight per thread.
@@ -750,6 +790,35 @@ cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t gro
                 else dense_kv_kernel<3><<<g2, threads, 0, st>>>(p4, P, pairs);
             } else {
                 launch_dense_kt<float>(k, reinterpret_cast<float2*>(psi), P, groups, grid, st);
+            }
+        }
+        return cudaGetLastError();
+    }
+    if (k == 4 || k == 5) {
+        // one group per thread, 128 threads per block; enough blocks for ~16 resident warps per SM
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 127) / 128, 148ull * 8));
+        // complex64 rows per loop iteration (profiles/r02_dense_wide.txt: 8 best; complex128: 2,
+        // its 2^5 inputs alone take 128 registers)
+        static const int unr = [] {
+            const char* e = getenv("SV_KW_UNROLL");
+            return e ? atoi(e) : 8;
+        }();
+        if (dbl) {
+            const auto& P = *reinterpret_cast<const DenseParams<double>*>(params);
+            double2* p2 = reinterpret_cast<double2*>(psi);
+            if (k == 4) dense_kw_kernel<double, 4, 2><<<grid, 128, 0, st>>>(p2, P, groups);
+            else dense_kw_kernel<double, 5, 2><<<grid, 128, 0, st>>>(p2, P, groups);
+        } else {
+            const auto& P = *reinterpret_cast<const DenseParams<float>*>(params);
+            float2* p2 = reinterpret_cast<float2*>(psi);
+            if (k == 4) {
+                if (unr == 2) dense_kw_kernel<float, 4, 2><<<grid, 128, 0, st>>>(p2, P, groups);
+                else if (unr == 8) dense_kw_kernel<float, 4, 8><<<grid, 128, 0, st>>>(p2, P, groups);
+                else dense_kw_kernel<float, 4, 4><<<grid, 128, 0, st>>>(p2, P, groups);
+            } else {
+                if (unr == 2) dense_kw_kernel<float, 5, 2><<<grid, 128, 0, st>>>(p2, P, groups);
+                else if (unr == 8) dense_kw_kernel<float, 5, 8><<<grid, 128, 0, st>>>(p2, P, groups);
+                else dense_kw_kernel<float, 5, 4><<<grid, 128, 0, st>>>(p2, P, groups);
             }
         }
         return cudaGetLastError();

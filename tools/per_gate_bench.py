@@ -35,7 +35,17 @@ Z = np.diag([1, -1]).astype(complex)
 rng = np.random.default_rng(0)
 q, _ = np.linalg.qr(rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)))
 U2 = q
-cases = [("H q0", H, [0], []), ("H q14", H, [14], []), ("H q29", H, [n - 1], []),
+def haar(k, seed):
+    r = np.random.default_rng(seed)
+    d = 1 << k
+    qq, _ = np.linalg.qr(r.normal(size=(d, d)) + 1j * r.normal(size=(d, d)))
+    return qq
+
+
+cases = [("dense U3 q1,q12,q27", haar(3, 3), [1, 12, n - 3], []),
+         ("dense U4 q0,q6,q13,q28", haar(4, 4), [0, 6, 13, n - 2], []),
+         ("dense U5 q2,q5,q11,q19,q29", haar(5, 5), [2, 5, 11, 19, n - 1], []),
+         ("H q0", H, [0], []), ("H q14", H, [14], []), ("H q29", H, [n - 1], []),
          ("T q7", T, [7], []), ("CZ q3,q20", Z, [20], [3]), ("CNOT q0->q29", X, [n - 1], [0]),
          ("CNOT q29->q1", X, [1], [n - 1]), ("Toffoli q2,q9->q25", X, [25], [2, 9]),
          ("dense U2 q5,q17", U2, [5, 17], [])]
