@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(256) dense_k_kernel(typename V2<real>::t* __re
 // Specialised dense-k for k = 1..3 (single gates, sv_apply_gate): compile-time group size
 // (the amplitudes stay in registers), two groups in flight per thread (g and g + T, both
 // coalesced across the warp), grid sized to the SMs.
-template <typename real, int K>
+template <typename real, int K, int G>
 __global__ void __launch_bounds__(256) dense_kt_kernel(typename V2<real>::t* __restrict__ psi,
                                                        const __grid_constant__ DenseParams<real> P,
                                                        uint64_t groups) {
@@ -414,30 +414,28 @@ __global__ void __launch_bounds__(256) dense_kt_kernel(typename V2<real>::t* __r
         }
         return base | P.cmask;
     };
-    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += 2 * T) {
-        const bool two = g + T < groups;
-        const uint64_t b0 = base_of(g), b1 = two ? base_of(g + T) : b0;
-        V x[D], y[D];
+    // G groups in flight per thread (g, g + T, ...: each coalesced across the warp)
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += G * T) {
+        V x[G][D];
+        uint64_t b[G];
 #pragma unroll
-        for (int c = 0; c < D; ++c) x[c] = psi[b0 + P.off[c]];
-        if (two) {
+        for (int i = 0; i < G; ++i) {
+            const uint64_t gi = g + i * T;
+            b[i] = base_of(gi < groups ? gi : g);
+            if (gi < groups) {
 #pragma unroll
-            for (int c = 0; c < D; ++c) y[c] = psi[b1 + P.off[c]];
+                for (int c = 0; c < D; ++c) x[i][c] = psi[b[i] + P.off[c]];
+            }
         }
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-            V acc = cmul(x[0], P.M[2 * (r * D)], P.M[2 * (r * D) + 1]);
-#pragma unroll
-            for (int c = 1; c < D; ++c) acc = cfma(acc, x[c], P.M[2 * (r * D + c)], P.M[2 * (r * D + c) + 1]);
-            psi[b0 + P.off[r]] = acc;
-        }
-        if (two) {
+        for (int i = 0; i < G; ++i) {
+            if (g + i * T >= groups) continue;
 #pragma unroll
             for (int r = 0; r < D; ++r) {
-                V acc = cmul(y[0], P.M[2 * (r * D)], P.M[2 * (r * D) + 1]);
+                V acc = cmul(x[i][0], P.M[2 * (r * D)], P.M[2 * (r * D) + 1]);
 #pragma unroll
-                for (int c = 1; c < D; ++c) acc = cfma(acc, y[c], P.M[2 * (r * D + c)], P.M[2 * (r * D + c) + 1]);
-                psi[b1 + P.off[r]] = acc;
+                for (int c = 1; c < D; ++c) acc = cfma(acc, x[i][c], P.M[2 * (r * D + c)], P.M[2 * (r * D + c) + 1]);
+                psi[b[i] + P.off[r]] = acc;
             }
         }
     }
@@ -486,7 +484,7 @@ __global__ void __launch_bounds__(128) dense_kw_kernel(typename V2<real>::t* __r
 // complex64 dense-k with qubit 0 free (no gate qubit on it): groups 2h and 2h+1 have bases
 // b and b+1, so one 16-byte load fetches the same matrix index of both groups; two such
 // group pairs in flight per thread.
-template <int K>
+template <int K, int G>
 __global__ void __launch_bounds__(256) dense_kv_kernel(float4* __restrict__ psi4,
                                                        const __grid_constant__ DenseParams<float> P,
                                                        uint64_t pairs) {
@@ -518,23 +516,26 @@ __global__ void __launch_bounds__(256) dense_kv_kernel(float4* __restrict__ psi4
 #pragma unroll
         for (int r = 0; r < D; ++r) x[r] = y[r];
     };
-    for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < pairs; h += 2 * T) {
-        const bool two = h + T < pairs;
-        const uint64_t b0 = base_of(2 * h), b1 = two ? base_of(2 * (h + T)) : b0;
-        float4 x[D], z[D];
+    // G group pairs in flight per thread (h, h + T, ..., h + (G-1) T: each coalesced across
+    // the warp), all loads issued before any arithmetic
+    for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < pairs; h += G * T) {
+        float4 x[G][D];
+        uint64_t b[G];
 #pragma unroll
-        for (int c = 0; c < D; ++c) x[c] = psi4[b0 + (P.off[c] >> 1)];
-        if (two) {
+        for (int i = 0; i < G; ++i) {
+            const uint64_t hi = h + i * T;
+            b[i] = base_of(2 * (hi < pairs ? hi : h));
+            if (hi < pairs) {
 #pragma unroll
-            for (int c = 0; c < D; ++c) z[c] = psi4[b1 + (P.off[c] >> 1)];
+                for (int c = 0; c < D; ++c) x[i][c] = psi4[b[i] + (P.off[c] >> 1)];
+            }
         }
-        apply(x);
 #pragma unroll
-        for (int r = 0; r < D; ++r) psi4[b0 + (P.off[r] >> 1)] = x[r];
-        if (two) {
-            apply(z);
+        for (int i = 0; i < G; ++i) {
+            if (h + i * T >= pairs) continue;
+            apply(x[i]);
 #pragma unroll
-            for (int r = 0; r < D; ++r) psi4[b1 + (P.off[r] >> 1)] = z[r];
+            for (int r = 0; r < D; ++r) psi4[b[i] + (P.off[r] >> 1)] = x[i][r];
         }
     }
 }
@@ -761,9 +762,12 @@ static unsigned grid_for(uint64_t work, int threads) {
 template <typename real>
 static void launch_dense_kt(int k, typename V2<real>::t* psi, const DenseParams<real>& P, uint64_t groups,
                             unsigned grid, cudaStream_t st) {
-    if (k == 1) dense_kt_kernel<real, 1><<<grid, 256, 0, st>>>(psi, P, groups);
-    else if (k == 2) dense_kt_kernel<real, 2><<<grid, 256, 0, st>>>(psi, P, groups);
-    else dense_kt_kernel<real, 3><<<grid, 256, 0, st>>>(psi, P, groups);
+    // groups in flight per thread (profiles/r02_per_gate.txt): K = 1: 4 (complex64) / 2
+    // (complex128), K = 2, 3: 2
+    if (k == 1 && sizeof(real) == 4) dense_kt_kernel<real, 1, 4><<<grid, 256, 0, st>>>(psi, P, groups);
+    else if (k == 1) dense_kt_kernel<real, 1, 2><<<grid, 256, 0, st>>>(psi, P, groups);
+    else if (k == 2) dense_kt_kernel<real, 2, 2><<<grid, 256, 0, st>>>(psi, P, groups);
+    else dense_kt_kernel<real, 3, 2><<<grid, 256, 0, st>>>(psi, P, groups);
 }
 
 cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t groups, cudaStream_t st) {
@@ -785,9 +789,9 @@ cudaError_t launch_dense_k(bool dbl, void* psi, const void* params, uint64_t gro
                 const uint64_t w2 = (pairs + 2 * threads - 1) / (2 * threads);
                 const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(w2, 148ull * 8));
                 float4* p4 = reinterpret_cast<float4*>(psi);
-                if (k == 1) dense_kv_kernel<1><<<g2, threads, 0, st>>>(p4, P, pairs);
-                else if (k == 2) dense_kv_kernel<2><<<g2, threads, 0, st>>>(p4, P, pairs);
-                else dense_kv_kernel<3><<<g2, threads, 0, st>>>(p4, P, pairs);
+                if (k == 1) dense_kv_kernel<1, 4><<<g2, threads, 0, st>>>(p4, P, pairs);
+                else if (k == 2) dense_kv_kernel<2, 2><<<g2, threads, 0, st>>>(p4, P, pairs);
+                else dense_kv_kernel<3, 2><<<g2, threads, 0, st>>>(p4, P, pairs);
             } else {
                 launch_dense_kt<float>(k, reinterpret_cast<float2*>(psi), P, groups, grid, st);
             }
