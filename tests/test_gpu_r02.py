@@ -215,3 +215,41 @@ def test_near_unit_custom_gates_keep_their_deviation(P):
         got = sv.amplitudes()
     ref = oracle.simulate(text)
     assert np.max(np.abs(got - ref)) <= 1e-12
+
+
+# ------------------------------------------------------------------ wide dense blocks at size
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("mode", [{}, {"force_kernel": 2}])
+def test_wide_dense_blocks_21q(P, dtype, mode):
+    """k = 4, 5 dense / controlled blocks at 21 q (dense-k kernels with many blocks and a
+    grid-stride tail; fused: OP_U4 in registers, k = 5 as dense passes) against the oracle."""
+    n = 21
+    c = W.random_circuit(n, 40, 2121, kinds=["U", "CU", "Udiag", "H", "CZ"], max_k=5, max_controls=2)
+    text = W.to_text(c)
+    psi0 = W.random_state(n, 21)
+    psi0 = W.round_to_c64(psi0) if dtype == "c64" else psi0
+    with P.StateVector(n, dtype) as sv:
+        sv.set_amplitudes(psi0)
+        sv.apply_circuit(text, **mode)
+        got = sv.amplitudes()
+    assert_close(got, oracle.simulate(text, psi0.astype(complex)), dtype, W.gate_count(c))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_apply_gate_wide_blocks_with_controls(P, dtype):
+    """sv_apply_gate with k = 4, 5 (dense_kw) with and without controls, targets unsorted and
+    including qubit 0."""
+    n = 18
+    psi0 = W.random_state(n, 4)
+    psi0 = W.round_to_c64(psi0) if dtype == "c64" else psi0
+    ref = psi0.astype(complex)
+    rng = np.random.default_rng(5)
+    with P.StateVector(n, dtype) as sv:
+        sv.set_amplitudes(psi0)
+        for k, tg, ct in ((4, [7, 0, 13, 2], []), (5, [17, 3, 0, 9, 11], []), (4, [1, 5, 6, 16], [0]),
+                          (5, [2, 4, 8, 10, 12], [15, 1])):
+            U = W.random_unitary(k, rng)
+            sv.apply_gate(U, tg, ct)
+            ref = oracle.apply_gate(ref, U, tg, ct)
+        got = sv.amplitudes()
+    assert_close(got, ref, dtype, 4)
