@@ -589,7 +589,7 @@ def run_ours(args):
     # e2e: same metric through the public API with host buffers: IR text in, parse + plan +
     # init + apply, marginal probabilities of 20 qubits (8 MiB fp64) back to the host.
     e2e_q = list(range(min(20, n)))
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(args.steps, 10))
     init()  # one untimed warm-up step (first call parses, plans and fills the plan cache)
     sv.apply_circuit(text)
     sv.probabilities(e2e_q)

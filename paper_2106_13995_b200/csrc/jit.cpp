@@ -1404,8 +1404,8 @@ std::string gen_pair_source(const PassPlan& A, const PassPlan& B, const PairGeom
       << ");\n";
     o << "__syncthreads();\nif(threadIdx.x==0){__threadfence();atomicAdd(done+c,1u);}\n";  // (RED: no wait)
     o << "}else{\n";
-    o << "if(threadIdx.x==0){unsigned v;for(;;){asm volatile(\"ld.acquire.gpu.global.u32 %0,[%1];\":\"=r\"(v):\"l\"(done+c):\"memory\");"
-         "if(v>=NA)break;__nanosleep(64);}__threadfence();}\n";
+    o << "if(threadIdx.x==0){unsigned v;const unsigned long long t0_=clock64();for(;;){asm volatile(\"ld.acquire.gpu.global.u32 %0,[%1];\":\"=r\"(v):\"l\"(done+c):\"memory\");"
+         "if(v>=NA)break;__nanosleep(64);if(clock64()-t0_>(1ull<<36))__trap();}__threadfence();}\n";  // ~35 s: a lost arrival traps instead of hanging
     o << "__syncthreads();\n";
     o << "tileB(psi,base|(" << deposit(geo.AmB, "j") << "),sm);\n";
     o << "}\n}\n}\n";
@@ -1459,9 +1459,11 @@ std::string gen_small_source(const std::vector<const PassPlan*>& ps, int variant
         const PassPlan& pp = *ps[i];
         if (i > 0) {
             // grid barrier: every CTA's stores of the previous pass before anyone's loads
-            o << "__syncthreads();\nif(threadIdx.x==0){__threadfence();atomicAdd(bar,1u);unsigned v;for(;;){"
+            // (a lost arrival traps after ~35 s of clock instead of hanging the GPU)
+            o << "__syncthreads();\nif(threadIdx.x==0){__threadfence();atomicAdd(bar,1u);unsigned v;"
+                 "const unsigned long long t0_=clock64();for(;;){"
                  "asm volatile(\"ld.acquire.gpu.global.u32 %0,[%1];\":\"=r\"(v):\"l\"(bar):\"memory\");if(v>="
-              << i << "u*gridDim.x)break;}__threadfence();}\n__syncthreads();\n";
+              << i << "u*gridDim.x)break;if(clock64()-t0_>(1ull<<36))__trap();}__threadfence();}\n__syncthreads();\n";
         }
         o << "for(unsigned long long tl_=blockIdx.x;tl_<" << pp.ntiles << "ull;tl_+=gridDim.x){\n";
         o << "unsigned long long base=tl_;\n";
