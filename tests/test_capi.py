@@ -90,3 +90,14 @@ def test_sharded_ex_argument_errors_before_any_cuda_call():
     for world, rank in ((3, 0), (16, 0), (2, 2)):
         assert lib.sv_create_sharded_ex(10, 1, ctypes.cast(uid, ctypes.c_void_p), None, world, rank, None, None,
                                         ctypes.byref(h)) == 1
+
+
+def test_check_unitary_option():
+    """sv_run_opts.check_unitary rejects a non-unitary matrix at plan time (SV_ERR_ARG with the
+    line); unchecked plans accept it (unitarity is not checked by default)."""
+    import paper_2106_13995_b200 as P
+    bad = "qubits: 2\nH 1\nU 0 : 1,0,1,0,0,0,1,0\n"
+    with pytest.raises(P.SvError, match="line 3.*not unitary"):
+        P.Plan(bad, "c64", check_unitary=True)
+    P.Plan(bad, "c64")
+    P.Plan("qubits: 2\nH 0\nU 1 : 0,0,1,0,1,0,0,0\n", "c128", check_unitary=True)
