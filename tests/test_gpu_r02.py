@@ -253,3 +253,40 @@ def test_apply_gate_wide_blocks_with_controls(P, dtype):
             ref = oracle.apply_gate(ref, U, tg, ct)
         got = sv.amplitudes()
     assert_close(got, ref, dtype, 4)
+
+
+def test_plan_cache_concurrent_threads(P):
+    """sv_apply_circuit's process-wide plan cache under concurrency: 4 host
+    threads, each with its own state, apply 24 distinct circuits (more than the 16 cached
+    plans, so entries are evicted while other threads use them) and one shared circuit;
+    every result matches the oracle."""
+    import threading
+    n = 10
+    texts = [W.to_text(W.random_circuit(n, 30, 900 + i, max_k=3)) for i in range(24)]
+    shared = W.to_text(W.supremacy(5, 2, 8, seed=9))
+    refs = [oracle.simulate(t) for t in texts]
+    ref_shared = oracle.simulate(shared)
+    errors = []
+
+    def work(tid):
+        try:
+            with P.StateVector(n, "c128") as sv:
+                for r in range(3):
+                    for i in range(tid, len(texts), 4):
+                        sv.init_zero()
+                        sv.apply_circuit(texts[i])
+                        if np.max(np.abs(sv.amplitudes() - refs[i])) > 1e-10:
+                            errors.append((tid, i))
+                        sv.init_zero()
+                        sv.apply_circuit(shared)
+                        if np.max(np.abs(sv.amplitudes() - ref_shared)) > 1e-10:
+                            errors.append((tid, "shared"))
+        except Exception as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[:5]
