@@ -568,20 +568,36 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if world > 1 and args.workload == "supremacy" and args.qubits == 30:
         args.workload = "supremacy36"  # BASELINE config 5 is the N > 1 workload
-    c, text, name = make_workload(args, world)
-    n = c.n
-    G = len(c.gates)
-    if world > 1:
-        sv = P.StateVector.sharded(n, args.dtype, control=args.control)
-    else:
-        sv = P.StateVector(n, args.dtype)
-
     def barrier():
         if world > 1:
             dist.barrier()
 
-    res = time_case(P, torch, sv, c, text, args.dtype, args.workload, args.steps, args.warmup, world, local,
-                    barrier)
+    # N > 1: if config 5 cannot be allocated on these GPUs (every rank sees the same failure:
+    # the state and its buffers are sized alike), fall back to the 33-qubit strong-scaling
+    # circuit and say so in the line, rather than print nothing
+    fallback = None
+    while True:
+        c, text, name = make_workload(args, world)
+        n = c.n
+        G = len(c.gates)
+        try:
+            if world > 1:
+                sv = P.StateVector.sharded(n, args.dtype, control=args.control)
+            else:
+                sv = P.StateVector(n, args.dtype)
+            res = time_case(P, torch, sv, c, text, args.dtype, args.workload, args.steps, args.warmup, world, local,
+                            barrier)
+            break
+        except P.SvError as e:
+            if world == 1 or args.workload != "supremacy36" or e.status != 3:  # 3 = SV_ERR_RESOURCE
+                raise
+            fallback = f"{name}: {e}"[:300]
+            try:
+                sv.close()
+            except Exception:
+                pass
+            args.workload = "strong33"
+            barrier()
     st, info, init = res["st"], res["info"], res["init"]
     ms_per_step = res["ms_per_step"]
     launches = res["launches"]
@@ -667,6 +683,7 @@ def run_ours(args):
                 "l2": "state (>= 8 GiB per GPU) is larger than L2 (126 MB): no flush needed",
                 "parallelism": f"sharded by top {g} qubits over {world} GPUs" if world > 1 else "single GPU",
                 "value_is": "circuit gates (IR gates, R12) / circuit wall time; whole job",
+                "fallback_from": fallback,
             },
             "circuit_wall_ms": ms_per_step,
             "hbm_gbs": res["achieved"],
