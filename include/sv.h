@@ -32,7 +32,9 @@
  *     Asynchronous CUDA/NCCL faults surface at the next synchronising call as SV_ERR_CUDA
  *     / SV_ERR_NCCL.  An error detected before any launch leaves the handle unchanged.
  *   - sv_last_error() returns a thread-local message for the last failing call.
- *   - A handle is single-writer.  Sharded handles are collective: every rank
+ *   - A state handle is single-writer; a plan may be applied to different states
+ *     from several threads (applies of one plan are serialised internally), and
+ *     sv_apply_circuit's process-wide plan cache is thread-safe.  Sharded handles are collective: every rank
  *     makes the same calls in the same order.
  */
 #ifndef SV_H_

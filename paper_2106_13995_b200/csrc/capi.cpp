@@ -689,6 +689,9 @@ sv_status sv_plan_destroy(sv_plan p) {
 
 sv_status sv_plan_apply(sv_state s, sv_plan p, sv_run_stats* stats) {
     if (!s || !p) return fail(SV_ERR_ARG, "NULL argument");
+    // a plan may be applied from several threads (to different states): its lazily built
+    // parts (schedule, kernels, sharded schedules, profiling events) are guarded by its mutex
+    std::lock_guard<std::mutex> plan_lock(p->mu);
     if (p->circ.n != s->n) return fail(SV_ERR_STATE, "plan width " + std::to_string(p->circ.n) +
                                                          " does not match state width " + std::to_string(s->n));
     if (p->dtype != s->dtype) return fail(SV_ERR_STATE, "plan dtype does not match state dtype");
@@ -818,10 +821,7 @@ sv_status sv_apply_circuit(sv_state s, const char* ir_text, const sv_run_opts* o
         while (cache.size() > 16) cache.pop_back();  // destroyed when its last user returns
     }
     if (p->circ.n != s->n) return fail(SV_ERR_STATE, "circuit width does not match the state");
-    {
-        std::lock_guard<std::mutex> lk(p->mu);
-        st = sv_plan_apply(s, p.get(), stats);
-    }
+    st = sv_plan_apply(s, p.get(), stats);  // (serialised per plan inside)
     const auto t1 = std::chrono::steady_clock::now();
     if (stats) stats->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     return st;
