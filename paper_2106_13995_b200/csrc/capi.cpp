@@ -652,7 +652,6 @@ sv_status sv_plan_shard_info(sv_plan p, int world, uint64_t* swaps, uint64_t* ba
     std::vector<int> phys(n);
     for (int q = 0; q < n; ++q) phys[q] = q;
     RunOpts o = p->opts;
-    if (o.force_kernel == SV_KERNEL_DENSE) o.force_kernel = SV_KERNEL_PER_GATE;
     ShardPlan sp;
     std::string err;
     const sv_status st = shard_plan(p->lcirc, o, n, nl, world, p->dtype == SV_C128, {0}, phys, sp, err);

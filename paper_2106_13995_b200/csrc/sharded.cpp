@@ -442,8 +442,9 @@ sv_status restore_borrowed(sv_state_s* s, std::string& err) {
 
 sv_status sharded_apply(sv_state_s* s, sv_plan_s* p, sv_run_stats* stats) {
     std::string err;
+    // (dense mode stays: lower_gate takes the dense-k kernels only for gates whose targets are
+    // local after the exchanges, the others defer to an exchange first or fold into rank constants)
     RunOpts o = p->opts;
-    if (o.force_kernel == SV_KERNEL_DENSE) o.force_kernel = SV_KERNEL_PER_GATE;  // dense-k needs local targets
     std::vector<int> ranks;
     for (int i = 0; i < nshards(s); ++i) ranks.push_back(rank_of(s, i));
     // plan cache: the schedule depends only on the map at entry, the shard ranks and dtype

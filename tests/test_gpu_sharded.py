@@ -236,3 +236,24 @@ def test_33q_p8_virtual_matches_single_gpu(P):
             l2 += float(np.sum(d * d))
     assert mx <= 1e-4
     assert np.sqrt(l2) <= 16 * G * 2.0 ** -24, np.sqrt(l2)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_sharded_apply_gate_dense_kernels(P, world, dtype):
+    """sv_apply_gate on sharded states uses the dense-k kernels for local targets (k = 1..5,
+    with local and global controls); gates with global targets exchange first."""
+    n = 14
+    psi0 = W.random_state(n, 40 + world)
+    psi0 = W.round_to_c64(psi0) if dtype == "c64" else psi0
+    rng = np.random.default_rng(world)
+    ref = psi0.astype(complex)
+    with P.StateVector.virtual_sharded(n, world, dtype) as sv:
+        sv.set_amplitudes(psi0)
+        for k, tg, ct in ((1, [0], []), (2, [3, 1], [13]), (3, [2, 5, 7], [0]), (4, [1, 4, 6, 9], []),
+                          (5, [0, 2, 3, 8, 10], [12]), (2, [13, 4], []), (1, [12], [0, 1])):
+            U = W.random_unitary(k, rng)
+            sv.apply_gate(U, tg, ct)
+            ref = oracle.apply_gate(ref, U, tg, ct)
+        got = sv.amplitudes()
+    assert_close(got, ref, dtype, 7)
