@@ -758,6 +758,16 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
     if (cm) e.o << "}\n";
 }
 
+// complex64 stores of the generated passes as st.{shared,global}.v2.f32 (SV_SPLIT_STORES=0:
+// plain 64-bit stores, which ptxas stages through a copied register pair)
+bool split_stores() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SPLIT_STORES");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
 // Shared-memory slot swizzle (GF(2)-linear, see sv_kernels.hpp).  With cp.async prefetch
 // (16-byte chunks) a complex64 slot pair must stay adjacent: the XOR then spares bit 0.
 uint32_t swz_mask(bool dbl, bool pf) { return dbl ? 7u : (pf ? 0xEu : 0xFu); }
@@ -877,6 +887,20 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             tpc *= 2;
     threads = tthreads * tpc;
     smem = pf ? 2 * tile_bytes : multi ? tile_bytes * tpc : 0;
+    // SV_CTA_CAP = C > 0: at most C resident CTAs per SM for passes at the default register
+    // width (dynamic shared memory padded so that C + 1 do not fit the 228 KiB per SM)
+    static const int cta_cap = [] {
+        const char* e = getenv("SV_CTA_CAP");
+        return e ? atoi(e) : -1;
+    }();
+    // default: 5 for complex64 (30 q supremacy c64: a pass whose registers allow 6 CTAs per SM
+    // streams HBM slower -- last pass 2.98 -> 2.50 ms with the cap, profiles/r03_cta_cap.txt);
+    // none for complex128 (4 CTAs per SM at its register width)
+    const int cap_eff = cta_cap >= 0 ? cta_cap : (sym.dbl ? 0 : 5);
+    if (cap_eff > 0 && multi && !pf && !md.device_fn && rb == (sym.dbl ? 4 : 5)) {
+        const size_t need = (size_t)233472 / (size_t)(cap_eff + 1) - 1024 + 1;
+        if (smem < need) smem = (need + 1023) / 1024 * 1024;
+    }
     int local_of[64];
     for (int i = 0; i < 64; ++i) local_of[i] = -1;
     for (int b = 0; b < m; ++b) local_of[sym.tq[b]] = b;
@@ -904,7 +928,12 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
              "DI C I(C a){return pk(-hi(a),lo(a));}\n"
              "DI C NI(C a){return pk(hi(a),-lo(a));}\n"
              "DI C SX(C a,C s){return a^(s&0x8000000080000000ull);}\n"
-             "DI C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}\n";
+             "DI C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}\n"
+             // stores as two 32-bit halves: with a b64 operand ptxas copies the pair into a
+             // staging pair (2 MOVs per store, one issue cycle each in an FP-bound pass)
+             "DI void SS(C* p,C v){asm volatile(\"st.shared.v2.f32 [%0],{%1,%2};\"::\"r\"((unsigned)__cvta_generic_to_shared(p)),"
+             "\"f\"(lo(v)),\"f\"(hi(v)):\"memory\");}\n"
+             "DI void SG(C* p,C v){asm volatile(\"st.global.v2.f32 [%0],{%1,%2};\"::\"l\"(p),\"f\"(lo(v)),\"f\"(hi(v)):\"memory\");}\n";
         // FFMA2 issues at 1/3 per cycle on B200, two scalar FFMAs at 1 each
         // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes
         o << (scalar_fma() ? "#define F F1\n" : "#define F F2\n");
@@ -1053,70 +1082,187 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         st_local[si] = tq_local;
     }
     // Shared-memory layout of each stage transition k (stage k writes, k+1 reads): slot
-    // swz_k(x) = x ^ sum_{p >= lb, x_p = 1} a_k[p], a GF(2)-linear XOR into the low lb slot bits
-    // (lb = log2 of the slots per 128-byte wavefront phase).  a_k is chosen so that the lanes
-    // of one phase (thread bits 0..lb-1) hit distinct banks for BOTH the writer and the reader.
+    // S_k(x) = XOR over the set local bits p of x of col_k[p], col_k[p] = 2^pi_k[p] ^ F_k[p]: a bit
+    // permutation pi_k plus a GF(2)-linear XOR F_k of bits placed high (pi >= lb) into the low
+    // lb slot bits (lb = log2 of the slots per 128-byte wavefront phase).  Conflict-free: the
+    // lanes of one phase (thread bits 0..lb-1) of the writer AND of the reader reach lb
+    // independent low images (distinct banks).  Additive (SV_ADD_LAYOUT, default): a register
+    // bit placed high with F = 0 contributes a slot bit no thread bit and no other register
+    // touches, so its offset is an ADD -- an immediate of the LDS/STS address -- and only the
+    // other ("XOR") register bits need run-time bases (2^|X| - 1 LOP3s per side instead of one
+    // per access: in an FP-bound pass every non-FP instruction costs an issue cycle,
+    // tools/micro/issue_mix.cu).  The search places lb bits low (preferring bits that are no
+    // register of either side) and draws F for the lanes placed high; a register of one side
+    // that is a lane of the other always costs one XOR bit.
     const int lbk = sym.dbl ? 3 : 4;
-    std::vector<std::vector<uint32_t>> swa(NS, std::vector<uint32_t>(m, 0));
+    static const bool add_layout = [] {
+        const char* e = getenv("SV_ADD_LAYOUT");
+        return e ? atoi(e) != 0 : true;
+    }();
+    struct Lay {
+        std::vector<int> pi;     // local bit -> slot bit
+        std::vector<uint32_t> F;  // local bit -> XOR into the low lb slot bits (pi >= lb only)
+        bool add = false;        // register offsets split into XOR bases + ADD immediates
+        uint32_t col(int p) const { return (1u << pi[p]) ^ F[p]; }
+        bool operator!=(const Lay& b) const { return pi != b.pi || F != b.F; }
+    };
+    std::vector<Lay> lay(NS);
+    for (auto& L : lay) {
+        L.pi.resize(m);
+        L.F.assign(m, 0);
+        for (int p = 0; p < m; ++p) L.pi[p] = p;
+    }
+    auto lanes_of = [&](size_t k) {
+        return std::vector<int>(st_local[k].begin(), st_local[k].begin() + std::min<size_t>(lbk, st_local[k].size()));
+    };
+    auto regs_of = [&](size_t k) {
+        std::vector<int> r;
+        for (int q : sym.stages[k].rq) r.push_back(local_of[q]);
+        return r;
+    };
+    // rank over GF(2) of the low images of the given local bits (lb x lb)
+    auto low_rank = [&](const Lay& L, const std::vector<int>& P) {
+        uint32_t basis[8] = {0};
+        int r = 0;
+        for (int p : P) {
+            uint32_t v = L.col(p) & ((1u << lbk) - 1);
+            for (int b = lbk - 1; b >= 0 && v; --b) {
+                if (!((v >> b) & 1)) continue;
+                if (!basis[b]) { basis[b] = v; ++r; v = 0; break; }
+                v ^= basis[b];
+            }
+        }
+        return r;
+    };
     for (size_t k = 0; k + 1 < NS; ++k) {
-        std::vector<uint32_t>& a = swa[k];
-        for (int p = lbk; p < m; ++p) a[p] = 1u << ((p - lbk) % lbk);
-        auto col = [&](int p) { return p < lbk ? (1u << p) : a[p]; };
-        auto full_rank = [&](const std::vector<int>& P) {
-            uint32_t basis[8] = {0};
-            int r = 0;
-            for (size_t i = 0; i < P.size() && (int)i < lbk; ++i) {
-                uint32_t v = col(P[i]);
-                for (int b = lbk - 1; b >= 0 && v; --b) {
-                    if (!((v >> b) & 1)) continue;
-                    if (!basis[b]) { basis[b] = v; ++r; v = 0; break; }
-                    v ^= basis[b];
+        const std::vector<int> Pw = lanes_of(k), Pr = lanes_of(k + 1);
+        if ((int)Pw.size() < lbk || (int)Pr.size() < lbk || pf) continue;
+        Lay& a = lay[k];
+        bool done = false;
+        if (add_layout) {
+            const std::vector<int> Wr = regs_of(k), Rr = regs_of(k + 1);
+            auto in = [](const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); };
+            // every lb-subset as the low set, cheapest lower bound first
+            std::vector<std::pair<int, uint32_t>> cand;
+            for (uint32_t low = 0; low < (1u << m); ++low) {
+                if (__builtin_popcount(low) != lbk) continue;
+                int xw = 0, xr = 0;
+                for (int p = 0; p < m; ++p) {
+                    const bool lo = (low >> p) & 1;
+                    if (in(Wr, p) && (lo || in(Pr, p))) ++xw;
+                    if (in(Rr, p) && (lo || in(Pw, p))) ++xr;
+                }
+                cand.push_back({(1 << xw) + (1 << xr), low});
+            }
+            std::stable_sort(cand.begin(), cand.end(),
+                             [](const std::pair<int, uint32_t>& x, const std::pair<int, uint32_t>& y) { return x.first < y.first; });
+            uint64_t rng = 0x9E3779B97F4A7C15ull ^ (k * 0x100000001B3ull);
+            for (size_t ci = 0; ci < cand.size() && !done; ++ci) {
+                const uint32_t low = cand[ci].second;
+                Lay t;
+                t.pi.resize(m);
+                t.F.assign(m, 0);
+                t.add = true;
+                int nl = 0, nh = lbk;
+                for (int p = 0; p < m; ++p) t.pi[p] = ((low >> p) & 1) ? nl++ : nh++;
+                std::vector<int> hl;  // lanes placed high: they need an F
+                for (int p : Pw) if (!((low >> p) & 1)) hl.push_back(p);
+                for (int p : Pr) if (!((low >> p) & 1) && !in(hl, p)) hl.push_back(p);
+                for (int tries = 0; tries < 400 && !done; ++tries) {
+                    for (int p : hl) {
+                        rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+                        t.F[p] = 1u + (uint32_t)(rng % ((1u << lbk) - 1));
+                    }
+                    if (low_rank(t, Pw) == lbk && low_rank(t, Pr) == lbk) { a = t; done = true; }
+                    if (hl.empty()) break;
                 }
             }
-            return r == lbk;
-        };
-        std::vector<int> Pw(st_local[k].begin(), st_local[k].begin() + std::min<size_t>(lbk, st_local[k].size()));
-        std::vector<int> Pr(st_local[k + 1].begin(),
-                            st_local[k + 1].begin() + std::min<size_t>(lbk, st_local[k + 1].size()));
-        // measured (profiles/r01_swizzle.txt): complex64 27.35 vs 28.14 ms; complex128 57.4
-        // vs 58.7 ms once its heaviest pass runs with 3 register bits (with 4 that pass slowed
-        // down on instruction fetch when its bank conflicts went away)
+        }
+        if (done) continue;
+        // XOR-only layout (identity placement): a_k[p] for the high bits, seeded search
+        for (int p = lbk; p < m; ++p) a.F[p] = 1u << ((p - lbk) % lbk);
         static const bool search = [] {
             const char* e = getenv("SV_SWZ_SEARCH");
             return e ? atoi(e) != 0 : true;
         }();
-        if (!search || pf || (int)Pw.size() < lbk || (int)Pr.size() < lbk || (full_rank(Pw) && full_rank(Pr)))
-            continue;
+        // measured (profiles/r01_swizzle.txt): complex64 27.35 vs 28.14 ms; complex128 57.4
+        // vs 58.7 ms once its heaviest pass runs with 3 register bits (with 4 that pass slowed
+        // down on instruction fetch when its bank conflicts went away)
+        if (!search || (low_rank(a, Pw) == lbk && low_rank(a, Pr) == lbk)) continue;
         std::vector<int> Q;
         for (int p : Pw) if (p >= lbk) Q.push_back(p);
         for (int p : Pr) if (p >= lbk && std::find(Q.begin(), Q.end(), p) == Q.end()) Q.push_back(p);
         uint64_t rng = 0x9E3779B97F4A7C15ull ^ (k * 0x100000001B3ull);
-        const std::vector<uint32_t> a0 = a;
+        const std::vector<uint32_t> a0 = a.F;
         bool ok = false;
         for (int tries = 0; tries < 20000 && !ok; ++tries) {
             for (int p : Q) {
                 rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
-                a[p] = 1u + (uint32_t)(rng % ((1u << lbk) - 1));
+                a.F[p] = 1u + (uint32_t)(rng % ((1u << lbk) - 1));
             }
-            ok = full_rank(Pw) && full_rank(Pr);
+            ok = low_rank(a, Pw) == lbk && low_rank(a, Pr) == lbk;
         }
-        if (!ok) a = a0;
+        if (!ok) a.F = a0;
     }
-    auto swz_k = [&](size_t k, uint32_t x) {
-        if (pf) return swz_const(x, sym.dbl, pf);
-        uint32_t y = x;
-        for (int p = lbk; p < m; ++p)
-            if ((x >> p) & 1) y ^= swa[k][p];
-        return y;
-    };
-    // run-time slot of the thread part: tl ^ sum over thread bits i (local position >= lb) of a_k
+    if (getenv("SV_LAYOUT_DEBUG"))
+        for (size_t k = 0; k + 1 < NS; ++k) {
+            fprintf(stderr, "T%zu add=%d W[", k, (int)lay[k].add);
+            for (int p : st_local[k]) fprintf(stderr, "%d ", p);
+            fprintf(stderr, "] Wr[");
+            for (int q : sym.stages[k].rq) fprintf(stderr, "%d ", local_of[q]);
+            fprintf(stderr, "] R[");
+            for (int p : st_local[k + 1]) fprintf(stderr, "%d ", p);
+            fprintf(stderr, "] Rr[");
+            for (int q : sym.stages[k + 1].rq) fprintf(stderr, "%d ", local_of[q]);
+            fprintf(stderr, "] col[");
+            for (int p = 0; p < m; ++p) fprintf(stderr, "%u ", lay[k].col(p));
+            fprintf(stderr, "]\n");
+        }
+    // run-time slot of the thread part of stage si under transition k's layout
     auto swz_thread = [&](size_t k, const std::vector<int>& tq_local) {
+        const Lay& L = lay[k];
+        std::vector<int> dst;
+        for (int p : tq_local) dst.push_back(L.pi[p]);
         std::ostringstream t;
-        t << "tl";
+        t << "(" << deposit_expr(dst, false) << ")";  // '|' binds looser than '^'
         for (size_t i = 0; i < tq_local.size(); ++i)
-            if (tq_local[i] >= lbk && swa[k][tq_local[i]])
-                t << "^((0u-((t>>" << i << ")&1u))&" << swa[k][tq_local[i]] << "u)";
+            if (L.F[tq_local[i]]) t << "^((0u-((t>>" << i << ")&1u))&" << L.F[tq_local[i]] << "u)";
         return t.str();
+    };
+    // shared-memory addresses of the R registers of stage si under transition k's layout:
+    // declares the XOR bases (named nm, nm1, ...) and returns the index expression per register
+    auto smem_addrs = [&](size_t k, size_t si, const std::string& nm) {
+        const Lay& L = lay[k];
+        const StageSym& st = sym.stages[si];
+        std::vector<std::string> ex(R);
+        uint32_t xmask = 0;  // register bits j that are XOR bits
+        for (int j = 0; j < rb; ++j) {
+            const int p = local_of[st.rq[j]];
+            if (!L.add || L.F[p] || L.pi[p] < lbk) xmask |= 1u << j;
+        }
+        std::map<uint32_t, std::string> base;  // XOR value -> variable
+        base[0] = nm;
+        for (int s = 0; s < R; ++s) {
+            uint32_t xv = 0, av = 0;
+            for (int j = 0; j < rb; ++j)
+                if ((s >> j) & 1) {
+                    const uint32_t c = L.col(local_of[st.rq[j]]);
+                    if ((xmask >> j) & 1) xv ^= c;
+                    else av |= c;
+                }
+            if (!L.add) {
+                ex[s] = nm + "^" + std::to_string(xv) + "u";
+                continue;
+            }
+            auto it = base.find(xv);
+            if (it == base.end()) {
+                const std::string v = nm + "_" + std::to_string(si) + "_" + std::to_string(base.size());
+                o << "const unsigned " << v << "=" << nm << "^" << xv << "u;";
+                it = base.emplace(xv, v).first;
+            }
+            ex[s] = av ? it->second + "+" + std::to_string(av) + "u" : it->second;
+        }
+        return ex;
     };
     for (size_t si = first; si < sym.stages.size(); ++si) {
         const StageSym& st = sym.stages[si];
@@ -1140,13 +1286,11 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             for (int j = 0; j < rb; ++j)
                 if ((s >> j) & 1) { go |= 1ull << st.rq[j]; lo |= 1u << local_of[st.rq[j]]; }
             goff[s] = go;
-            loff[s] = pf ? swz_const(lo, sym.dbl, pf) : (si > 0 ? swz_k(si - 1, lo) : 0);
-            loffw[s] = pf ? loff[s] : (writes_smem ? swz_k(si, lo) : 0);
+            if (pf) loff[s] = loffw[s] = swz_const(lo, sym.dbl, pf);
         }
         if (reads_smem || writes_smem) {
-            const std::string tl = deposit_expr(tq_local, false);
-            o << "tl=" << tl << ";\n";
             if (pf) {
+                o << "tl=" << deposit_expr(tq_local, false) << ";\n";
                 const int lb = sym.dbl ? 3 : 4;
                 o << "{unsigned y=tl>>" << lb << ", f=0; while(y){f^=y&" << ((1u << lb) - 1) << "u; y>>=" << lb
                   << ";} tl^=f&" << smask << "u;}\n";
@@ -1175,7 +1319,12 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             o << "\n";
         } else {
             if (si > first) o << "__syncthreads();\n";
-            for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[tr^" << loff[s] << "u];";
+            if (pf) {
+                for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[tr^" << loff[s] << "u];";
+            } else {
+                const std::vector<std::string> ad = smem_addrs(si - 1, si, "tr");
+                for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[" << ad[s] << "];";
+            }
             o << "\n";
         }
         for (const LOp& op : st.ops) emit_op(e, op, sc, ps);
@@ -1270,6 +1419,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             if (xS < 0) {
                 for (int s = 0; s < R; ++s) {
                     if (stream_hints()) o << "STS_(psi+g+" << goff[s] << "ull," << reg(s) << ");";
+                    else if (!sym.dbl && split_stores()) o << "SG(psi+g+" << goff[s] << "ull," << reg(s) << ");";
                     else o << "psi[g+" << goff[s] << "ull]=" << reg(s) << ";";
                 }
             } else {
@@ -1300,8 +1450,16 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             // a stage that read the buffer in the previous transition's layout and writes it in
             // a different one must wait for every thread's reads first (its slots are other
             // threads' sources)
-            if (!pf && si > first && reads_smem && swa[si - 1] != swa[si]) o << "__syncthreads();\n";
-            for (int s = 0; s < R; ++s) o << SM << "[tw^" << loffw[s] << "u]=" << reg(s) << ";";
+            if (!pf && si > first && reads_smem && lay[si - 1] != lay[si]) o << "__syncthreads();\n";
+            std::vector<std::string> ad(R);
+            if (pf)
+                for (int s = 0; s < R; ++s) ad[s] = "tw^" + std::to_string(loffw[s]) + "u";
+            else
+                ad = smem_addrs(si, si, "tw");
+            for (int s = 0; s < R; ++s) {
+                if (!sym.dbl && split_stores()) o << "SS(" << SM << "+(" << ad[s] << ")," << reg(s) << ");";
+                else o << SM << "[" << ad[s] << "]=" << reg(s) << ";";
+            }
             o << "\n";
         }
     }
