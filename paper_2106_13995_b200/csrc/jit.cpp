@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <sstream>
 #include <thread>
+#include <functional>
 #include <unordered_map>
 
 #include "jit.hpp"
@@ -38,6 +39,16 @@ struct Em {
     bool dbl = false;
     std::map<std::string, std::string> rk;  // per-thread run-time constants already declared
     std::set<std::string> pure_signs;       // run-time values that are exactly +-1
+    // run-time real factors as selections: value = (-1)^(xor of sconds) * prod (cond ? a : b).
+    // A multiplier k * value is then declared as a select of constants (equal halves), which
+    // ptxas issues as FFMA2 with a broadcast 32-bit (or uniform) operand -- 2 cycles on the FMA
+    // pipe instead of 3 for a packed register multiplier (tools/micro/issue_mix.cu)
+    struct Sel {
+        std::vector<std::string> sconds;
+        std::vector<std::tuple<std::string, double, double>> fac;
+    };
+    std::map<std::string, Sel> sel;
+    uint64_t tile_mask = ~0ull;  // physical qubits of the pass's tile (others are tile-base bits)
     int nvar = 0;
 
     std::string lit(double v) const {
@@ -128,6 +139,30 @@ std::string scaled(const Em& e, const std::string& v, const cd& c) {
 // kept pending per register like the unit phases and folded into the next reader as the
 // multiplier of an FFMA2/FMUL2 (free when the reader is a butterfly); products with matrix
 // entries are per-thread constants declared once.
+// k * (run-time factor sl) as a select tree of constants ("" if it has too many factors)
+std::string sel_expr(const Em& e, const Em::Sel& sl, double k) {
+    if (sl.fac.size() > 2) return std::string();
+    std::string sc;
+    for (const std::string& c : sl.sconds) sc += (sc.empty() ? "" : "^") + std::string("(") + c + ")";
+    auto leaf = [&](double v) { return e.dbl ? e.lit(v) : k2(v, v); };
+    // nested selects over the factor conditions, signed leaves
+    std::function<std::string(size_t, double)> tree = [&](size_t i, double v) -> std::string {
+        if (i == sl.fac.size()) return leaf(v);
+        const auto& f = sl.fac[i];
+        return "((" + std::get<0>(f) + ")?" + tree(i + 1, v * std::get<1>(f)) + ":" + tree(i + 1, v * std::get<2>(f)) + ")";
+    };
+    if (sc.empty()) return tree(0, k);
+    return "((" + sc + ")?" + tree(0, -k) + ":" + tree(0, k) + ")";
+}
+
+bool sel_consts() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SEL_CONSTS");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
 std::string rt_const(Em& e, double k, const std::string& r) {
     if (k == 1.0) return r;
     if (k == -1.0) return e.dbl ? "(-" + r + ")" : "N(" + r + ")";
@@ -135,7 +170,10 @@ std::string rt_const(Em& e, double k, const std::string& r) {
     auto it = e.rk.find(key);
     if (it != e.rk.end()) return it->second;
     const std::string name = "rk" + std::to_string(e.nvar++);
-    if (e.dbl) e.o << "const R " << name << "=" << r << "*" << e.lit(k) << ";";
+    auto si = e.sel.find(r);
+    const std::string sx = (sel_consts() && si != e.sel.end()) ? sel_expr(e, si->second, k) : std::string();
+    if (!sx.empty()) e.o << (e.dbl ? "const R " : "const C ") << name << "=" << sx << ";";
+    else if (e.dbl) e.o << "const R " << name << "=" << r << "*" << e.lit(k) << ";";
     else e.o << "const C " << name << "=M(" << r << "," << k2(k, k) << ");";
     e.rk.emplace(key, name);
     return name;
@@ -263,24 +301,47 @@ void flush_ph(Em& e, PassState& ps, int s) {
 }
 
 // a new per-thread sign (+-1 by a run-time condition)
-std::string make_sign(Em& e, const std::string& cond, double c_true, double c_false) {
-    const std::string name = "sg" + std::to_string(e.nvar++);
+std::string make_sign(Em& e, const std::string& cond, double c_true, double c_false,
+                      const char* prefix = "sg") {
+    const std::string name = prefix + std::to_string(e.nvar++);
     if (e.dbl) e.o << "const R " << name << "=(" << cond << ")?" << e.lit(c_true) << ":" << e.lit(c_false) << ";";
     else e.o << "const C " << name << "=(" << cond << ")?" << k2(c_true, c_true) << ":" << k2(c_false, c_false) << ";";
+    Em::Sel sl;
+    if (c_true == -1.0 && c_false == 1.0) sl.sconds.push_back(cond);
+    else if (c_true == 1.0 && c_false == -1.0) sl.sconds.push_back("!(" + cond + ")");
+    else sl.fac.emplace_back(cond, c_true, c_false);
+    e.sel[name] = sl;
     if (std::abs(c_true) == 1.0 && std::abs(c_false) == 1.0) e.pure_signs.insert(name);
     return name;
+}
+
+// condition "physical index bit q is 1": a tile-base bit reads the CTA's base (uniform over
+// the CTA: ptxas keeps selects on it in uniform registers), a tile bit reads g
+std::string bit_cond(const Em& e, int q) {
+    const bool tile = (e.tile_mask >> q) & 1;
+    return std::string("((") + (tile ? "g" : "base") + ">>" + std::to_string(q) + ")&1ull)";
 }
 
 // product of two run-time signs (empty = +1), declared once per pass
 std::string sign_mul(Em& e, PassState& ps, const std::string& a, const std::string& b) {
     if (a.empty()) return b;
     if (b.empty()) return a;
-    if (a == b) return std::string();
+    if (a == b && e.pure_signs.count(a)) return std::string();
     const std::string key = a < b ? a + "*" + b : b + "*" + a;
     auto it = ps.sgprod.find(key);
     if (it == ps.sgprod.end()) {
         const std::string name = "sg" + std::to_string(e.nvar++);
-        if (e.dbl) e.o << "const R " << name << "=" << a << "*" << b << ";";
+        auto sa = e.sel.find(a), sb = e.sel.find(b);
+        std::string sx;
+        if (sel_consts() && sa != e.sel.end() && sb != e.sel.end()) {
+            Em::Sel sl = sa->second;
+            sl.sconds.insert(sl.sconds.end(), sb->second.sconds.begin(), sb->second.sconds.end());
+            sl.fac.insert(sl.fac.end(), sb->second.fac.begin(), sb->second.fac.end());
+            sx = sel_expr(e, sl, 1.0);
+            if (!sx.empty()) e.sel[name] = sl;
+        }
+        if (!sx.empty()) e.o << (e.dbl ? "const R " : "const C ") << name << "=" << sx << ";";
+        else if (e.dbl) e.o << "const R " << name << "=" << a << "*" << b << ";";
         else e.o << "const C " << name << "=M(" << a << "," << b << ");";
         if (e.pure_signs.count(a) && e.pure_signs.count(b)) e.pure_signs.insert(name);
         it = ps.sgprod.emplace(key, name).first;
@@ -530,7 +591,7 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
         const int q = op.dq[0], pq = sc.pos[q];
         if (cm || pq < 0) {
             std::string cond = cm ? "((g&" + std::to_string(cm) + "ull)==" + std::to_string(cm) + "ull)" : "true";
-            if (pq < 0) cond += "&&((g>>" + std::to_string(q) + ")&1ull)";
+            if (pq < 0) cond += "&&" + bit_cond(e, q);
             const std::string sg = make_sign(e, cond, -1, 1);
             for (int s : touched) {
                 if (pq >= 0 && !((s >> pq) & 1)) continue;
@@ -690,8 +751,7 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
                                     std::abs(c1.real()) == 1.0;
             if (q >= 0 && pq < 0 && real_signs && !cm) {
                 // +-1 chosen by a non-register index bit: a pending run-time sign
-                const std::string sg =
-                    make_sign(e, "((g>>" + std::to_string(q) + ")&1ull)", c1.real(), c0.real());
+                const std::string sg = make_sign(e, bit_cond(e, q), c1.real(), c0.real());
                 for (int s : touched) add_sign(e, ps, s, sg);
                 e.o << "\n";
             } else if (q >= 0 && pq < 0) {
@@ -870,6 +930,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                             const GenMode* mode) {
     Em e;
     e.dbl = sym.dbl;
+    e.tile_mask = 0;
+    for (int q : sym.tq) e.tile_mask |= 1ull << q;
     const GenMode md = mode ? *mode : GenMode();
     const int rb = sym.rb, R = 1 << rb;
     const int m = (int)sym.tq.size();
@@ -894,7 +956,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         return e ? atoi(e) : -1;
     }();
     // default: 5 for complex64 (30 q supremacy c64: a pass whose registers allow 6 CTAs per SM
-    // streams HBM slower -- last pass 2.98 -> 2.50 ms with the cap, profiles/r03_cta_cap.txt);
+    // streams HBM slower -- last pass 2.98 -> 2.50 ms with the cap, profiles/r03_layout_ab.txt);
     // none for complex128 (4 CTAs per SM at its register width)
     const int cap_eff = cta_cap >= 0 ? cta_cap : (sym.dbl ? 0 : 5);
     if (cap_eff > 0 && multi && !pf && !md.device_fn && rb == (sym.dbl ? 4 : 5)) {
@@ -1362,10 +1424,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                 if (sc.pos[kv.first] >= 0) continue;
                 const cd s0 = kv.second.first, s1 = kv.second.second;
                 if (s0.imag() == 0.0 && s1.imag() == 0.0) {
-                    const std::string k = "ks" + std::to_string(e.nvar++);
-                    const std::string cond = "((g>>" + std::to_string(kv.first) + ")&1ull)";
-                    if (e.dbl) o << "const R " << k << "=" << cond << "?" << e.lit(s1.real()) << ":" << e.lit(s0.real()) << ";";
-                    else o << "const C " << k << "=" << cond << "?" << k2(s1.real(), s1.real()) << ":" << k2(s0.real(), s0.real()) << ";";
+                    const std::string k = make_sign(e, bit_cond(e, kv.first), s1.real(), s0.real(), "ks");
                     rscale = sign_mul(e, ps, rscale, k);
                 } else {
                     rt.push_back(kv.first);

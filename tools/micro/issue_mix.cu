@@ -31,6 +31,10 @@ __global__ void k(u64* out, u64 seed, float fs) {
     for (int i = 0; i < NCH; ++i) { v[i] = seed + i + threadIdx.x; f[i] = fs + i + threadIdx.x; dd[i] = f[i]; }
     const double ds = fs * 0.5;
     const u64 kk = seed * 3;
+    const unsigned wid = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const u64 kw = (wid & 1) ? 0xbf3504f3bf3504f3ull : 0x3f3504f33f3504f3ull;
+    // block-uniform multiplier (uniform datapath candidate): derived from blockIdx only
+    const u64 ku = (blockIdx.x & 1) ? 0xbf3504f3bf3504f3ull : 0x3f3504f33f3504f3ull;
     for (int it = 0; it < ITER; ++it) {
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
@@ -63,6 +67,9 @@ __global__ void k(u64* out, u64 seed, float fs) {
             if (MODE == 25) { sts(sbase + i * 264, v[(i + 3) % NCH]); }
             if (MODE == 26) { v[i] = A(v[i], kk); u[i] = lds(sbase + i * 264); u[(i + 4) % NCH] = lds(sbase + ((i + 4) % NCH) * 264 + 8); }
             if (MODE == 27) { v[i] = A(v[i], kk); w[i] = mov(w[(i + 1) % NCH]); }
+            if (MODE == 28) v[i] = F(v[i], kk, v[(i + 1) % NCH]);
+            if (MODE == 29) v[i] = F(v[i], ku, v[(i + 1) % NCH]);
+            if (MODE == 30) v[i] = F(v[i], kw, v[(i + 1) % NCH]);
             if (MODE == 21) { w[i] = iadd(w[i], w[(i + 1) % NCH]); }
         }
     }
@@ -123,5 +130,8 @@ int main() {
     run<26>("FADD2+LDS.64 1:2", d);
     run<24>("LDS.64 alone", d);
     run<27>("FADD2+MOV 1:1", d);
+    run<28>("FFMA2 (param mult)", d);
+    run<29>("FFMA2 (block-uniform mult)", d);
+    run<30>("FFMA2 (warp-uniform via shfl)", d);
     return 0;
 }
