@@ -818,6 +818,16 @@ void emit_op(Em& e, const LOp& op, const StageCtx& sc, PassState& ps) {
     if (cm) e.o << "}\n";
 }
 
+// complex64 stage transitions through 16-byte shared-memory accesses where a register bit sits
+// at slot bit 0 (two amplitudes per LDS.128 / STS.128; SV_PAIR_SMEM=0: 8-byte accesses only)
+bool pair_smem() {
+    static const bool b = [] {
+        const char* e = getenv("SV_PAIR_SMEM");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return b;
+}
+
 // complex64 stores of the generated passes as st.{shared,global}.v2.f32 (SV_SPLIT_STORES=0:
 // plain 64-bit stores, which ptxas stages through a copied register pair)
 bool split_stores() {
@@ -995,6 +1005,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
              // staging pair (2 MOVs per store, one issue cycle each in an FP-bound pass)
              "DI void SS(C* p,C v){asm volatile(\"st.shared.v2.f32 [%0],{%1,%2};\"::\"r\"((unsigned)__cvta_generic_to_shared(p)),"
              "\"f\"(lo(v)),\"f\"(hi(v)):\"memory\");}\n"
+             "DI void SS2(C* p,C a,C b){asm volatile(\"st.shared.v4.f32 [%0],{%1,%2,%3,%4};\"::\"r\"((unsigned)__cvta_generic_to_shared(p)),"
+             "\"f\"(lo(a)),\"f\"(hi(a)),\"f\"(lo(b)),\"f\"(hi(b)):\"memory\");}\n"
              "DI void SG(C* p,C v){asm volatile(\"st.global.v2.f32 [%0],{%1,%2};\"::\"l\"(p),\"f\"(lo(v)),\"f\"(hi(v)):\"memory\");}\n";
         // FFMA2 issues at 1/3 per cycle on B200, two scalar FFMAs at 1 each
         // (tools/micro/fp_rate.cu), but the scalar form doubles the code of FMA-heavy passes
@@ -1165,6 +1177,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         std::vector<int> pi;     // local bit -> slot bit
         std::vector<uint32_t> F;  // local bit -> XOR into the low lb slot bits (pi >= lb only)
         bool add = false;        // register offsets split into XOR bases + ADD immediates
+        int p0 = -1;             // local bit at slot bit 0 that pairs registers (16-byte accesses)
         uint32_t col(int p) const { return (1u << pi[p]) ^ F[p]; }
         bool operator!=(const Lay& b) const { return pi != b.pi || F != b.F; }
     };
@@ -1183,11 +1196,12 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         return r;
     };
     // rank over GF(2) of the low images of the given local bits (lb x lb)
-    auto low_rank = [&](const Lay& L, const std::vector<int>& P) {
+    auto low_rank = [&](const Lay& L, const std::vector<int>& P, uint32_t bits = 0) {
         uint32_t basis[8] = {0};
         int r = 0;
+        if (!bits) bits = (1u << lbk) - 1;
         for (int p : P) {
-            uint32_t v = L.col(p) & ((1u << lbk) - 1);
+            uint32_t v = L.col(p) & bits;
             for (int b = lbk - 1; b >= 0 && v; --b) {
                 if (!((v >> b) & 1)) continue;
                 if (!basis[b]) { basis[b] = v; ++r; v = 0; break; }
@@ -1204,38 +1218,67 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         if (add_layout) {
             const std::vector<int> Wr = regs_of(k), Rr = regs_of(k + 1);
             auto in = [](const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); };
-            // every lb-subset as the low set, cheapest lower bound first
-            std::vector<std::pair<int, uint32_t>> cand;
-            for (uint32_t low = 0; low < (1u << m); ++low) {
-                if (__builtin_popcount(low) != lbk) continue;
-                int xw = 0, xr = 0;
-                for (int p = 0; p < m; ++p) {
-                    const bool lo = (low >> p) & 1;
-                    if (in(Wr, p) && (lo || in(Pr, p))) ++xw;
-                    if (in(Rr, p) && (lo || in(Pw, p))) ++xr;
+            const std::vector<int> W4 = lanes_of(k), R4 = lanes_of(k + 1);
+            // candidates: (pair bit p0 or -1, low set containing p0), by instruction count of
+            // both sides: R (R/2 when the side pairs its registers into 16-byte accesses) plus
+            // 2^|X| - 1 XOR bases.  The count depends on the placement only (an F goes to the
+            // lanes placed high, which are XOR bits exactly when they are registers of the
+            // other side); the F draw below only decides feasibility (no bank conflicts).
+            struct Cand { int cost; int p0; uint32_t low; };
+            std::vector<Cand> cand;
+            std::vector<int> p0s = {-1};
+            if (!sym.dbl && pair_smem())
+                for (int p = 0; p < m; ++p)
+                    if (in(Wr, p) || in(Rr, p)) p0s.push_back(p);
+            for (int p0 : p0s) {
+                const bool pw = p0 >= 0 && in(Wr, p0), pr = p0 >= 0 && in(Rr, p0);
+                const std::vector<int> Wl(W4.begin(), W4.begin() + (pw ? lbk - 1 : lbk));
+                const std::vector<int> Rl(R4.begin(), R4.begin() + (pr ? lbk - 1 : lbk));
+                if (p0 >= 0 && !pw && !in(Wl, p0)) continue;  // the unpaired side needs p0 as a lane
+                if (p0 >= 0 && !pr && !in(Rl, p0)) continue;
+                for (uint32_t low = 0; low < (1u << m); ++low) {
+                    if (__builtin_popcount(low) != lbk || (p0 >= 0 && !((low >> p0) & 1))) continue;
+                    int xw = 0, xr = 0;
+                    for (int p = 0; p < m; ++p) {
+                        const bool lo = (low >> p) & 1;
+                        if (in(Wr, p) && !(pw && p == p0) && (lo || in(Rl, p))) ++xw;
+                        if (in(Rr, p) && !(pr && p == p0) && (lo || in(Wl, p))) ++xr;
+                    }
+                    cand.push_back({(pw ? R / 2 : R) + (pr ? R / 2 : R) + (1 << xw) + (1 << xr), p0, low});
                 }
-                cand.push_back({(1 << xw) + (1 << xr), low});
             }
-            std::stable_sort(cand.begin(), cand.end(),
-                             [](const std::pair<int, uint32_t>& x, const std::pair<int, uint32_t>& y) { return x.first < y.first; });
+            std::stable_sort(cand.begin(), cand.end(), [](const Cand& x, const Cand& y) { return x.cost < y.cost; });
             uint64_t rng = 0x9E3779B97F4A7C15ull ^ (k * 0x100000001B3ull);
             for (size_t ci = 0; ci < cand.size() && !done; ++ci) {
-                const uint32_t low = cand[ci].second;
+                const uint32_t low = cand[ci].low;
+                const int p0 = cand[ci].p0;
+                const bool pw = p0 >= 0 && in(Wr, p0), pr = p0 >= 0 && in(Rr, p0);
+                const std::vector<int> Wl(W4.begin(), W4.begin() + (pw ? lbk - 1 : lbk));
+                const std::vector<int> Rl(R4.begin(), R4.begin() + (pr ? lbk - 1 : lbk));
                 Lay t;
                 t.pi.resize(m);
                 t.F.assign(m, 0);
                 t.add = true;
-                int nl = 0, nh = lbk;
-                for (int p = 0; p < m; ++p) t.pi[p] = ((low >> p) & 1) ? nl++ : nh++;
-                std::vector<int> hl;  // lanes placed high: they need an F
-                for (int p : Pw) if (!((low >> p) & 1)) hl.push_back(p);
-                for (int p : Pr) if (!((low >> p) & 1) && !in(hl, p)) hl.push_back(p);
+                t.p0 = p0;
+                int nl = p0 >= 0 ? 1 : 0, nh = lbk;
+                for (int p = 0; p < m; ++p) t.pi[p] = p == p0 ? 0 : ((low >> p) & 1) ? nl++ : nh++;
+                std::vector<int> hl;  // needed lanes placed high: they get an F
+                for (int p : Wl) if (!((low >> p) & 1)) hl.push_back(p);
+                for (int p : Rl) if (!((low >> p) & 1) && !in(hl, p)) hl.push_back(p);
+                // a paired side's slot bit 0 is its pair bit alone: F stays clear of bit 0
+                const uint32_t fm = p0 >= 0 ? ((1u << lbk) - 2) : ((1u << lbk) - 1);
+                const uint32_t bw = pw ? fm : (1u << lbk) - 1, br = pr ? fm : (1u << lbk) - 1;
                 for (int tries = 0; tries < 400 && !done; ++tries) {
                     for (int p : hl) {
-                        rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
-                        t.F[p] = 1u + (uint32_t)(rng % ((1u << lbk) - 1));
+                        do {
+                            rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+                            t.F[p] = (uint32_t)(rng % (1u << lbk)) & fm;
+                        } while (!t.F[p]);
                     }
-                    if (low_rank(t, Pw) == lbk && low_rank(t, Pr) == lbk) { a = t; done = true; }
+                    if (low_rank(t, Wl, bw) == (pw ? lbk - 1 : lbk) && low_rank(t, Rl, br) == (pr ? lbk - 1 : lbk)) {
+                        a = t;
+                        done = true;
+                    }
                     if (hl.empty()) break;
                 }
             }
@@ -1293,13 +1336,20 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     };
     // shared-memory addresses of the R registers of stage si under transition k's layout:
     // declares the XOR bases (named nm, nm1, ...) and returns the index expression per register
-    auto smem_addrs = [&](size_t k, size_t si, const std::string& nm) {
+    // jpair (out): the register bit paired into 16-byte accesses (its partner sits at slot + 1),
+    // -1 if none
+    auto smem_addrs = [&](size_t k, size_t si, const std::string& nm, int& jpair) {
         const Lay& L = lay[k];
         const StageSym& st = sym.stages[si];
         std::vector<std::string> ex(R);
+        jpair = -1;
         uint32_t xmask = 0;  // register bits j that are XOR bits
         for (int j = 0; j < rb; ++j) {
             const int p = local_of[st.rq[j]];
+            if (L.add && p == L.p0) {
+                jpair = j;
+                continue;
+            }
             if (!L.add || L.F[p] || L.pi[p] < lbk) xmask |= 1u << j;
         }
         std::map<uint32_t, std::string> base;  // XOR value -> variable
@@ -1307,11 +1357,12 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         for (int s = 0; s < R; ++s) {
             uint32_t xv = 0, av = 0;
             for (int j = 0; j < rb; ++j)
-                if ((s >> j) & 1) {
+                if (((s >> j) & 1) && j != jpair) {
                     const uint32_t c = L.col(local_of[st.rq[j]]);
                     if ((xmask >> j) & 1) xv ^= c;
                     else av |= c;
                 }
+            if (jpair >= 0 && ((s >> jpair) & 1)) av |= 1u;  // the partner slot
             if (!L.add) {
                 ex[s] = nm + "^" + std::to_string(xv) + "u";
                 continue;
@@ -1384,8 +1435,14 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             if (pf) {
                 for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[tr^" << loff[s] << "u];";
             } else {
-                const std::vector<std::string> ad = smem_addrs(si - 1, si, "tr");
-                for (int s = 0; s < R; ++s) o << reg(s) << "=" << SM << "[" << ad[s] << "];";
+                int jp;
+                const std::vector<std::string> ad = smem_addrs(si - 1, si, "tr", jp);
+                for (int s = 0; s < R; ++s) {
+                    if (jp < 0) o << reg(s) << "=" << SM << "[" << ad[s] << "];";
+                    else if (!((s >> jp) & 1))
+                        o << "{const ulonglong2 w_=*(const ulonglong2*)(" << SM << "+(" << ad[s] << "));" << reg(s)
+                          << "=w_.x;" << reg(s | (1 << jp)) << "=w_.y;}";
+                }
             }
             o << "\n";
         }
@@ -1511,12 +1568,16 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             // threads' sources)
             if (!pf && si > first && reads_smem && lay[si - 1] != lay[si]) o << "__syncthreads();\n";
             std::vector<std::string> ad(R);
+            int jp = -1;
             if (pf)
                 for (int s = 0; s < R; ++s) ad[s] = "tw^" + std::to_string(loffw[s]) + "u";
             else
-                ad = smem_addrs(si, si, "tw");
+                ad = smem_addrs(si, si, "tw", jp);
             for (int s = 0; s < R; ++s) {
-                if (!sym.dbl && split_stores()) o << "SS(" << SM << "+(" << ad[s] << ")," << reg(s) << ");";
+                if (jp >= 0) {
+                    if (!((s >> jp) & 1))
+                        o << "SS2(" << SM << "+(" << ad[s] << ")," << reg(s) << "," << reg(s | (1 << jp)) << ");";
+                } else if (!sym.dbl && split_stores()) o << "SS(" << SM << "+(" << ad[s] << ")," << reg(s) << ");";
                 else o << SM << "[" << ad[s] << "]=" << reg(s) << ";";
             }
             o << "\n";

@@ -43,6 +43,8 @@ static inline C NI(C a){return pk(hi(a),-lo(a));}
 static inline C SX(C a,C s){return a^(s&0x8000000080000000ull);}
 static inline C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}
 static inline void SS(C* p,C v){*p=v;}
+static inline void SS2(C* p,C a,C b){p[0]=a;p[1]=b;}
+struct ulonglong2 { unsigned long long x, y; };
 static inline void SG(C* p,C v){*p=v;}
 """
 
