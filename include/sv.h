@@ -189,7 +189,9 @@ sv_status sv_plan_compile(const char* ir_text, sv_dtype dtype, const sv_run_opts
 sv_status sv_plan_info(sv_plan p, int* n, uint64_t* gates, uint64_t* passes, uint64_t* stages);
 /* Generated CUDA source of tile pass `pass` of the single-GPU schedule (inspection and
  * profiling).  Writes at most cap bytes (NUL-terminated) and the full length to *len.
- * Returns SV_ERR_RANGE for a bad pass index; an empty string for a non-tile pass. */
+ * Returns SV_ERR_RANGE for a bad pass index; an empty string for a non-tile pass.  With the
+ * environment variable SV_SOURCE_VARIANT=basis (uniform), pass 0 is returned in its variant
+ * that synthesises a basis state (the uniform superposition) instead of loading its input. */
 sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len);
 sv_status sv_plan_destroy(sv_plan p);
 /* Logical -> physical qubit map the single-GPU schedule leaves (a relabelling schedule stores

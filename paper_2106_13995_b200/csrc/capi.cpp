@@ -629,7 +629,10 @@ sv_status sv_plan_source(sv_plan p, int pass, char* buf, size_t cap, size_t* len
     if (pp.kind == PassPlan::TILE && pp.sym) {
         jit_carries(p->sched);
         cd out;
-        src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers, tpc, false, -1, false, pp.carry_in,
+        // SV_SOURCE_VARIANT=basis|uniform: the first pass's fused-init variant (inspection)
+        const char* v = getenv("SV_SOURCE_VARIANT");
+        const bool vb = pass == 0 && v && !strcmp(v, "basis"), vu = pass == 0 && v && !strcmp(v, "uniform");
+        src = gen_pass_source(*pp.sym, pp.ntiles, threads, smem, pers, tpc, vb, -1, vu, pp.carry_in,
                               pp.carry_next ? &out : nullptr);
     }
     else if (pp.kind == PassPlan::PERM) src = gen_perm_source(pp, pp.perm_dbl, threads);

@@ -859,6 +859,16 @@ bool prefetch_enabled() {
     return b;
 }
 
+// SV_PERSIST=1: tile passes as persistent kernels (grid = resident CTAs, each CTA loops over
+// tiles), no CTA launch/teardown per tile
+bool persist_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_PERSIST");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
 bool scalar_fma() {
     static const bool b = [] {
         const char* e = getenv("SV_SCALAR_FMA");
@@ -958,6 +968,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                (!multi || tile_bytes * tpc * 2 <= (size_t)200 * 1024))
             tpc *= 2;
     threads = tthreads * tpc;
+    const bool ploop = !pf && !md.device_fn && xS < 0 && tpc == 1 && persist_enabled();
+    if (ploop) persistent = true;
     smem = pf ? 2 * tile_bytes : multi ? tile_bytes * tpc : 0;
     // SV_CTA_CAP = C > 0: at most C resident CTAs per SM for passes at the default register
     // width (dynamic shared memory padded so that C + 1 do not fit the 228 KiB per SM)
@@ -1101,6 +1113,9 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         o << "base=tile;\n";
     } else if (!md.device_fn) {
         if (tpc > 1) o << "base=(unsigned long long)blockIdx.x*" << tpc << "u+(threadIdx.x>>" << tb << ");\n";
+        else if (ploop)
+            o << "for(unsigned long long tile_=blockIdx.x;tile_<" << ntiles << "ull;tile_+=gridDim.x){\n"
+              << "__syncthreads();\nbase=tile_;\n";  // the previous tile's readers are done
         else o << "base=blockIdx.x;\n";
     }
     if (!md.device_fn)
@@ -1126,6 +1141,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     }
     const std::string SM = pf ? "bc" : "sm";
     PassState ps;
+    bool prescale = false;  // a synthesised input carries the deferred scale s0
+    double s0 = 1.0;
     ps.fac = carry_in;  // global phase left pending by the previous pass of the schedule
     ps.ph.assign(R, cd(1, 0));
     ps.rs.assign(R, std::string());
@@ -1415,16 +1432,28 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             }
         }
         if (!reads_smem && basis_in) {
-            // the pass input is the basis state |kb>: synthesise the tile, read nothing
-            const std::string one = sym.dbl ? "mk(1.0,0.0)" : "0x000000003f800000ull";
+            // the pass input is the basis state |kb>: synthesise the tile, read nothing.  Every
+            // register starts at zero; the one thread holding |kb> (kb ^ g has no bit outside its
+            // register positions) sets that register -- a branch no other warp takes.  The value
+            // is the pass's deferred scale S0 (SV_ONE_, fixed at the end of generation), so the
+            // final multiply by it disappears (the pass is linear).
             const std::string zero = sym.dbl ? "mk(0.0,0.0)" : "0ull";
-            for (int s = 0; s < R; ++s)
-                o << reg(s) << "=(kb==(g|" << goff[s] << "ull))?" << one << ":" << zero << ";";
-            o << "\n";
+            uint64_t rmask = 0;
+            for (int s = 0; s < R; ++s) rmask |= goff[s];
+            // register index of |kb> in this thread (its register bits gathered), or 0xff
+            o << "{const unsigned long long d_=kb^g;const unsigned ix_=((d_&" << ~rmask << "ull)==0ull)?(0u";
+            for (int j = 0; j < rb; ++j) o << "|((unsigned)(d_>>" << st.rq[j] << ")&1u)<<" << j;
+            o << "):0xffu;";
+            for (int s = 0; s < R; ++s) o << reg(s) << "=(ix_==" << s << "u)?SV_ONE_:" << zero << ";";
+            o << "}\n";
+            prescale = true;
         } else if (!reads_smem && uniform_in) {
-            // the pass input is the uniform superposition: every amplitude is u0, read nothing
-            for (int s = 0; s < R; ++s) o << reg(s) << "=u0;";
-            o << "\n";
+            // the pass input is the uniform superposition: every amplitude is u0 (times the
+            // deferred scale S0, as for the basis input), read nothing
+            o << "{const C us_=" << (sym.dbl ? "mk(u0.x*SV_S0R_,u0.y*SV_S0R_)" : "M(u0,SV_S0P_)") << ";";
+            for (int s = 0; s < R; ++s) o << reg(s) << "=us_;";
+            o << "}\n";
+            prescale = true;
         } else if (!reads_smem) {
             for (int s = 0; s < R; ++s)
                 o << reg(s) << (md.ldcg ? "=LDG(psi+g+" : stream_hints() ? "=LDS_(psi+g+" : "=psi[g+") << goff[s]
@@ -1509,6 +1538,14 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                     }
                 }
             }
+            if (prescale) {
+                // the synthesised input already carries S0 = |fac|
+                const double mag = std::abs(ps.fac);
+                if (std::isnormal(mag) && std::isnormal((float)mag)) {
+                    s0 = sym.dbl ? mag : (double)(float)mag;
+                    ps.fac /= s0;
+                }
+            }
             for (int s = 0; s < R; ++s) {
                 cd c = ps.fac;
                 for (auto& kv : ps.pend) c *= ((s >> sc.pos[kv.first]) & 1) ? kv.second.second : kv.second.first;
@@ -1584,8 +1621,19 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         }
     }
     if (pf) o << "__syncthreads(); {C* tmp=bc; bc=bn; bn=tmp;}\n}\n";
+    if (ploop) o << "}\n";
     o << "}\n";
-    return o.str();
+    std::string src = o.str();
+    if (prescale) {
+        // the deferred scale s0 of a synthesised input (see the first stage)
+        auto subst = [&](const std::string& tok, const std::string& val) {
+            for (size_t q; (q = src.find(tok)) != std::string::npos;) src.replace(q, tok.size(), val);
+        };
+        subst("SV_ONE_", sym.dbl ? "mk(" + e.lit(s0) + ",0.0)" : k2(s0, 0.0));
+        subst("SV_S0R_", e.lit(s0));
+        subst("SV_S0P_", k2(s0, s0));
+    }
+    return src;
 }
 
 // ------------------------------------------------------------------ pass pairs through L2
@@ -2055,7 +2103,7 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
         }
     }
     size_t basis_smem = 0;
-    if (first && first->jit_persistent) {  // persistent launch shape: no basis variant
+    if (first && first->jit_persistent && prefetch_enabled()) {  // prefetching pass: no basis variant
         first = nullptr;
         srcs.pop_back();
     }

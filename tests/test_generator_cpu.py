@@ -138,3 +138,36 @@ def test_merged_single_qubit_runs(P, dtype, n, seed):
     psi = W.round_to_c64(psi) if dtype == "c64" else psi
     got, _ = _emulated(P, text, n, dtype, psi)
     assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("k", [0, 5, 12345])
+def test_basis_input_variant(P, dtype, k, monkeypatch):
+    """The first pass's fused-init variant (synthesises |k> in registers, pre-scaled by the
+    pass's deferred factor) against the generic pass reading a stored |k>, and the whole plan
+    against the oracle."""
+    from tools.emulate import run_pass_on_host
+    n = 14
+    c = W.supremacy(4, 4, 12, seed=5, n=n)
+    text = W.to_text(c)
+    plan = P.Plan(text, dtype)
+    cdt = np.complex64 if dtype == "c64" else np.complex128
+    generic = plan.source(0)
+    monkeypatch.setenv("SV_SOURCE_VARIANT", "basis")
+    fused = plan.source(0)
+    monkeypatch.delenv("SV_SOURCE_VARIANT")
+    assert fused != generic and "kb" in fused
+    a = np.zeros(1 << n, dtype=cdt)
+    a[k] = 1
+    run_pass_on_host(generic, a, n)
+    b = np.full(1 << n, np.nan, dtype=cdt)  # the fused variant reads nothing
+    run_pass_on_host(fused, b, n, basis=k)
+    tol = 1e-6 if dtype == "c64" else 1e-14
+    assert np.max(np.abs(a - b)) <= tol * max(1.0, np.max(np.abs(a)))
+    # the rest of the plan after the fused first pass matches the oracle
+    for i in range(1, plan.info()["passes"]):
+        run_pass_on_host(plan.source(i), b, n)
+    got = to_logical(b, plan.qubit_map(), n)
+    psi = np.zeros(1 << n, dtype=np.complex128)
+    psi[k] = 1
+    assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))

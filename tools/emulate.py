@@ -62,7 +62,7 @@ _RUNNER = r"""
 #include <thread>
 #include <vector>
 struct Dim { unsigned x; };
-static thread_local Dim threadIdx, blockIdx;
+static thread_local Dim threadIdx, blockIdx, gridDim;
 static thread_local C* g_sm;
 static std::barrier<>* g_bar;
 static inline void __syncthreads() { g_bar->arrive_and_wait(); }
@@ -78,6 +78,7 @@ extern "C" int emu_run(void* psi, unsigned long long grid, int threads, unsigned
             th.emplace_back([&, t, b]() {
                 threadIdx.x = (unsigned)t;
                 blockIdx.x = (unsigned)b;
+                gridDim.x = (unsigned)grid;
                 g_sm = smem.data();
                 svpass((C*)psi EXTRA_ARG);
             });
