@@ -978,7 +978,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         return e ? atoi(e) : -1;
     }();
     // default: 5 for complex64 (30 q supremacy c64: a pass whose registers allow 6 CTAs per SM
-    // streams HBM slower -- last pass 2.98 -> 2.50 ms with the cap, profiles/r03_layout_ab.txt);
+    // streams HBM slower -- last pass 2.98 -> 2.50 ms with the cap, profiles/r02_layout_ab.txt);
     // none for complex128 (4 CTAs per SM at its register width)
     const int cap_eff = cta_cap >= 0 ? cta_cap : (sym.dbl ? 0 : 5);
     if (cap_eff > 0 && multi && !pf && !md.device_fn && rb == (sym.dbl ? 4 : 5)) {

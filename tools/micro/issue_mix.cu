@@ -26,6 +26,7 @@ __global__ void k(u64* out, u64 seed, float fs) {
     u64 u[NCH];
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm) + (threadIdx.x & 31) * 8;
     for (int i = 0; i < NCH; ++i) u[i] = i;
+    const unsigned bcast = (unsigned)__cvta_generic_to_shared(sm) + 2048;
     float f[NCH];
     double dd[NCH];
     for (int i = 0; i < NCH; ++i) { v[i] = seed + i + threadIdx.x; f[i] = fs + i + threadIdx.x; dd[i] = f[i]; }
@@ -70,6 +71,9 @@ __global__ void k(u64* out, u64 seed, float fs) {
             if (MODE == 28) v[i] = F(v[i], kk, v[(i + 1) % NCH]);
             if (MODE == 29) v[i] = F(v[i], ku, v[(i + 1) % NCH]);
             if (MODE == 30) v[i] = F(v[i], kw, v[(i + 1) % NCH]);
+            if (MODE == 31) v[i] = A(v[i], lds(bcast + i * 8));
+            if (MODE == 32) { v[i] = A(v[i], kk); v[(i + 4) % NCH] = A(v[(i + 4) % NCH], lds(bcast + i * 8)); }
+            if (MODE == 33) v[i] = A(v[i], lds(sbase + i * 264));
             if (MODE == 21) { w[i] = iadd(w[i], w[(i + 1) % NCH]); }
         }
     }
@@ -131,6 +135,9 @@ int main() {
     run<24>("LDS.64 alone", d);
     run<27>("FADD2+MOV 1:1", d);
     run<28>("FFMA2 (param mult)", d);
+    run<31>("FADD2(lds bcast) 1:1", d);
+    run<32>("FADD2+FADD2(lds bcast) 2:1", d);
+    run<33>("FADD2(lds 256B) 1:1", d);
     run<29>("FFMA2 (block-uniform mult)", d);
     run<30>("FFMA2 (warp-uniform via shfl)", d);
     return 0;
