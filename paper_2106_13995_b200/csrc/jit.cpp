@@ -2168,8 +2168,16 @@ sv_status jit_prepare(Schedule& sc, std::string& err, bool with_basis) {
         todo[i]->jit_fn = fns[i];
         if (todo[i]->jit_persistent) {
             int per_sm = 0, nsm = 148;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fns[i], todo[i]->jit_threads,
-                                                          todo[i]->jit_smem);
+            const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, (const void*)fns[i], todo[i]->jit_threads, todo[i]->jit_smem);
+            if (oe != cudaSuccess) cudaGetLastError();
+            static const int forced = [] {
+                const char* e = getenv("SV_PERSIST_CTAS");
+                return e ? atoi(e) : 0;
+            }();
+            if (forced > 0) per_sm = forced;
+            if (getenv("SV_PERSIST_DEBUG"))
+                fprintf(stderr, "persistent pass: %d CTAs/SM (occupancy query %s)\n", per_sm, cudaGetErrorString(oe));
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
             const uint64_t grid = (uint64_t)std::max(1, per_sm) * nsm;
             todo[i]->jit_grid = (unsigned)std::min<uint64_t>(grid, todo[i]->ntiles);

@@ -716,6 +716,19 @@ bool balance_enabled() {
 // Rollout tie-break by the modelled time (SV_ROLLOUT_BALANCE; default: complex64 only).
 // Measured (profiles/r01_rollout.txt): c64 30 q supremacy 24.08-24.12 -> 23.92 ms (same 7
 // passes, lighter heavy passes); c128: the balanced choice ends in 8 passes instead of 7.
+// op-cost units the FP pipe retires in one HBM pass (SV_MODEL_H).  87 when the
+// heavy passes ran at 76-81 % FMA-pipe occupancy; after the issue-slot work of late round 2
+// (fewer non-FP instructions per op) one HBM pass hides more: 30 q supremacy c64, interleaved
+// medians of 4 (profiles/r02_layout_ab.txt): 22.22 ms at 87/92, 21.84 at 100, 21.80 at 108,
+// 22.00 at 115, 22.10 at 130
+double model_h() {
+    static const double h = [] {
+        const char* e = getenv("SV_MODEL_H");
+        return e ? atof(e) : 108.0;
+    }();
+    return h;
+}
+
 bool rollout_balance(bool dbl) {
     static const int b = [] {
         const char* e = getenv("SV_ROLLOUT_BALANCE");
@@ -875,7 +888,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                 for (int idx : po) c += op_cost(ops[idx]);
                 return c;
             };
-            const double Hfull = 87.0;
+            const double Hfull = model_h();
             const double H0 = out.passes.empty() ? Hfull / 2 : Hfull;
             auto model = [&](double budget_cap, double& obj, size_t& npass) -> bool {
                 std::vector<int> po, de;
@@ -1219,7 +1232,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
                             if (pp2.sym)
                                 for (const StageSym& st : pp2.sym->stages)
                                     for (const LOp& op : st.ops) c += op_cost(op);
-                            model += std::max(c, 87.0);
+                            model += std::max(c, model_h());
                         }
                     np[k] = s2.passes.size();
                     mdl[k] = model;
