@@ -1141,8 +1141,6 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     }
     const std::string SM = pf ? "bc" : "sm";
     PassState ps;
-    bool prescale = false;  // a synthesised input carries the deferred scale s0
-    double s0 = 1.0;
     ps.fac = carry_in;  // global phase left pending by the previous pass of the schedule
     ps.ph.assign(R, cd(1, 0));
     ps.rs.assign(R, std::string());
@@ -1432,11 +1430,10 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             }
         }
         if (!reads_smem && basis_in) {
-            // the pass input is the basis state |kb>: synthesise the tile, read nothing.  Every
-            // register starts at zero; the one thread holding |kb> (kb ^ g has no bit outside its
-            // register positions) sets that register -- a branch no other warp takes.  The value
-            // is the pass's deferred scale S0 (SV_ONE_, fixed at the end of generation), so the
-            // final multiply by it disappears (the pass is linear).
+            // the pass input is the basis state |kb>: synthesise the tile, read nothing: a
+            // one-hot of the thread's register index of |kb> (its register bits of kb ^ g
+            // gathered; 0xff when kb is not one of this thread's amplitudes).  The value is
+            // exactly 1, so the pass gives bit for bit what it gives on a stored |kb>.
             const std::string zero = sym.dbl ? "mk(0.0,0.0)" : "0ull";
             uint64_t rmask = 0;
             for (int s = 0; s < R; ++s) rmask |= goff[s];
@@ -1444,16 +1441,13 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             o << "{const unsigned long long d_=kb^g;const unsigned ix_=((d_&" << ~rmask << "ull)==0ull)?(0u";
             for (int j = 0; j < rb; ++j) o << "|((unsigned)(d_>>" << st.rq[j] << ")&1u)<<" << j;
             o << "):0xffu;";
-            for (int s = 0; s < R; ++s) o << reg(s) << "=(ix_==" << s << "u)?SV_ONE_:" << zero << ";";
+            const std::string one = sym.dbl ? "mk(1.0,0.0)" : "0x000000003f800000ull";
+            for (int s = 0; s < R; ++s) o << reg(s) << "=(ix_==" << s << "u)?" << one << ":" << zero << ";";
             o << "}\n";
-            prescale = true;
         } else if (!reads_smem && uniform_in) {
-            // the pass input is the uniform superposition: every amplitude is u0 (times the
-            // deferred scale S0, as for the basis input), read nothing
-            o << "{const C us_=" << (sym.dbl ? "mk(u0.x*SV_S0R_,u0.y*SV_S0R_)" : "M(u0,SV_S0P_)") << ";";
-            for (int s = 0; s < R; ++s) o << reg(s) << "=us_;";
-            o << "}\n";
-            prescale = true;
+            // the pass input is the uniform superposition: every amplitude is u0, read nothing
+            for (int s = 0; s < R; ++s) o << reg(s) << "=u0;";
+            o << "\n";
         } else if (!reads_smem) {
             for (int s = 0; s < R; ++s)
                 o << reg(s) << (md.ldcg ? "=LDG(psi+g+" : stream_hints() ? "=LDS_(psi+g+" : "=psi[g+") << goff[s]
@@ -1538,14 +1532,6 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
                     }
                 }
             }
-            if (prescale) {
-                // the synthesised input already carries S0 = |fac|
-                const double mag = std::abs(ps.fac);
-                if (std::isnormal(mag) && std::isnormal((float)mag)) {
-                    s0 = sym.dbl ? mag : (double)(float)mag;
-                    ps.fac /= s0;
-                }
-            }
             for (int s = 0; s < R; ++s) {
                 cd c = ps.fac;
                 for (auto& kv : ps.pend) c *= ((s >> sc.pos[kv.first]) & 1) ? kv.second.second : kv.second.first;
@@ -1623,17 +1609,7 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
     if (pf) o << "__syncthreads(); {C* tmp=bc; bc=bn; bn=tmp;}\n}\n";
     if (ploop) o << "}\n";
     o << "}\n";
-    std::string src = o.str();
-    if (prescale) {
-        // the deferred scale s0 of a synthesised input (see the first stage)
-        auto subst = [&](const std::string& tok, const std::string& val) {
-            for (size_t q; (q = src.find(tok)) != std::string::npos;) src.replace(q, tok.size(), val);
-        };
-        subst("SV_ONE_", sym.dbl ? "mk(" + e.lit(s0) + ",0.0)" : k2(s0, 0.0));
-        subst("SV_S0R_", e.lit(s0));
-        subst("SV_S0P_", k2(s0, s0));
-    }
-    return src;
+    return o.str();
 }
 
 // ------------------------------------------------------------------ pass pairs through L2

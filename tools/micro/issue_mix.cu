@@ -31,6 +31,8 @@ __global__ void k(u64* out, u64 seed, float fs) {
     double dd[NCH];
     for (int i = 0; i < NCH; ++i) { v[i] = seed + i + threadIdx.x; f[i] = fs + i + threadIdx.x; dd[i] = f[i]; }
     const double ds = fs * 0.5;
+    const double dsu = (blockIdx.x & 1) ? -0.7071067811865476 : 0.7071067811865476;  // block-uniform
+    const double dsel = (threadIdx.x & 1) ? -0.7071067811865476 : 0.7071067811865476;  // per-thread select
     const u64 kk = seed * 3;
     const unsigned wid = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
     const u64 kw = (wid & 1) ? 0xbf3504f3bf3504f3ull : 0x3f3504f33f3504f3ull;
@@ -74,6 +76,9 @@ __global__ void k(u64* out, u64 seed, float fs) {
             if (MODE == 31) v[i] = A(v[i], lds(bcast + i * 8));
             if (MODE == 32) { v[i] = A(v[i], kk); v[(i + 4) % NCH] = A(v[(i + 4) % NCH], lds(bcast + i * 8)); }
             if (MODE == 33) v[i] = A(v[i], lds(sbase + i * 264));
+            if (MODE == 34) dd[i] = dd[i] * 0.7071067811865476 + dd[(i + 1) % NCH];
+            if (MODE == 35) dd[i] = dd[i] * dsu + dd[(i + 1) % NCH];
+            if (MODE == 36) dd[i] = dd[i] * dsel + dd[(i + 1) % NCH];
             if (MODE == 21) { w[i] = iadd(w[i], w[(i + 1) % NCH]); }
         }
     }
@@ -136,6 +141,9 @@ int main() {
     run<27>("FADD2+MOV 1:1", d);
     run<28>("FFMA2 (param mult)", d);
     run<31>("FADD2(lds bcast) 1:1", d);
+    run<34>("DFMA (imm const)", d);
+    run<35>("DFMA (block-uniform mult)", d);
+    run<36>("DFMA (per-thread select mult)", d);
     run<32>("FADD2+FADD2(lds bcast) 2:1", d);
     run<33>("FADD2(lds 256B) 1:1", d);
     run<29>("FFMA2 (block-uniform mult)", d);
