@@ -273,6 +273,28 @@ sv_status plan_schedule(sv_plan_s* p) {
     }
     const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err, &p->lcirc);
     if (st != SV_OK) return fail(st, err);
+    // complex64: tiles whose low positions form 128-byte runs (4 qubits) instead of 256-byte
+    // ones (5) have one more free qubit; take that plan when it needs fewer passes (a 30 q
+    // supremacy d20 circuit: 6 passes instead of 7, 21.8 -> 21.4 ms; the shorter runs cost
+    // ~1 % of HBM bandwidth, tools/micro/seg_bw.cu)
+    if (!ctx.dbl && p->opts.use_jit() && p->opts.tile_qubits == 0 && !getenv("SV_LOW_QUBITS") && ctx.nl >= 14 &&
+        p->sched.passes.size() > 1) {
+        RunOpts o4 = p->opts;
+        o4.low_qubits = 4;
+        std::vector<LOp> ops4;
+        for (size_t i = 0; i < p->lcirc.gates.size(); ++i) {
+            bool needs_global = false;
+            if (lower_gate(p->lcirc.gates[i], (int)i, ctx, o4, ops4, needs_global, err) != SV_OK) {
+                ops4.clear();
+                break;
+            }
+        }
+        Schedule s4;
+        if (!ops4.empty() && build_schedule(ops4, ctx, o4, s4, err, &p->lcirc) == SV_OK &&
+            s4.passes.size() < p->sched.passes.size())
+            p->sched = std::move(s4);
+        err.clear();
+    }
     // a reversible circuit: one gather pass, unless its scattered reads cost more than the
     // fused tile passes (both estimated in HBM passes)
     if (have_perm) {

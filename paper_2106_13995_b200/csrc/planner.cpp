@@ -682,8 +682,10 @@ double heavy_pass_cost(bool dbl) {
     static double b = [] {
         const char* e = getenv("SV_HEAVY_COST");
         // measured (profiles/r01_heavy_sweep.txt, after the 1-qubit merge): 30 q supremacy
-        // c64 25.9 ms at 200, 24.5 at 160, 24.8 at 130, 25.8 at 100
-        return e ? atof(e) : 160.0;
+        // c64 25.9 ms at 200, 24.5 at 160, 24.8 at 130, 25.8 at 100.  Late round 2 (smaller
+        // code per op): the 6-pass plan's 175-unit pass runs 4.76 ms with one register bit
+        // fewer and 4.52 ms without (profiles/r02_layout_ab.txt): 180
+        return e ? atof(e) : 180.0;
     }();
     static double b2 = [] {
         const char* e = getenv("SV_HEAVY_COST128");
@@ -770,7 +772,13 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
         return e ? atoi(e) : 0;
     }();
     const int m_pad = std::min(rb + 8, nl);       // single-stage passes: 256 threads
-    const int L = std::min(dbl ? 4 : 5, nl);      // low qubits: contiguous 256-byte runs
+    static const int env_low = [] {
+        const char* e = getenv("SV_LOW_QUBITS");
+        return e ? atoi(e) : 0;
+    }();
+    // low qubits: contiguous 256-byte runs (SV_LOW_QUBITS overrides; plan_schedule may ask for
+    // 128-byte runs when that saves a pass)
+    const int L = std::min(env_low > 0 ? env_low : o.low_qubits > 0 ? o.low_qubits : (dbl ? 4 : 5), nl);
     const uint64_t lowmask = (L >= 64) ? ~0ull : ((1ull << L) - 1);
     const bool per_gate = !o.fuse || o.force_kernel == SV_KERNEL_PER_GATE || o.force_kernel == SV_KERNEL_DENSE;
     // Relabelling (single GPU, generated kernels): the pass stores its tile with a permutation

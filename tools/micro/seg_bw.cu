@@ -43,17 +43,19 @@ int main() {
     const int n = 30;
     u64* psi; cudaMalloc(&psi, (1ull << n) * 8); cudaMemset(psi, 0, (1ull << n) * 8);
     int his[4][12] = {{12, 13, 14, 15, 16, 17, 18}, {19, 20, 21, 22, 23, 24, 25}, {5, 12, 13, 14, 15, 16}, {5, 6, 12, 13, 14, 15}};
-    const char* nm[6] = {"L=5 hi 12-18", "L=5 hi 19-25", "L=6 hi 12-16", "L=7 hi 12-16", "L=5 hi 24-29,17", "L=7 hi 24-28"};
-    Geo gs[6];
+    const char* nm[8] = {"L=5 hi 12-18", "L=5 hi 19-25", "L=6 hi 12-16", "L=7 hi 12-16", "L=5 hi 24-29,17", "L=7 hi 24-28", "L=3 hi 12-20", "L=4 hi 12-19"};
+    Geo gs[8];
     gs[0] = {{12, 13, 14, 15, 16, 17, 18}, 7, 5};
     gs[1] = {{19, 20, 21, 22, 23, 24, 25}, 7, 5};
     gs[2] = {{12, 13, 14, 15, 16, 17}, 6, 6};
     gs[3] = {{12, 13, 14, 15, 16}, 5, 7};
     gs[4] = {{17, 24, 25, 26, 27, 28, 29}, 7, 5};
     gs[5] = {{24, 25, 26, 27, 28}, 5, 7};
+    gs[6] = {{12, 13, 14, 15, 16, 17, 18, 19, 20}, 9, 3};
+    gs[7] = {{12, 13, 14, 15, 16, 17, 18, 19}, 8, 4};
     (void)his;
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-    for (int k = 0; k < 6; ++k) {
+    for (int k = 0; k < 8; ++k) {
         // positions of the hi list are bit-insertion order relative to the shifted base: adjust
         Geo G = gs[k];
         for (int r = 0; r < 2; ++r) pass<<<(1u << (n - 12)), 128>>>(psi, G);
