@@ -32,7 +32,11 @@ with P.StateVector(c.n, a.dtype) as sv:
     sv.sync()
 print(st, plan.info())
 
-# per-pass device times of a back-to-back run (CUDA events between launches)
+# per-pass device times of a back-to-back run (CUDA events between launches); RUN_PLAN_COOL=s
+# idles s seconds first (A/B runs under power capping: every variant starts from the same state)
+if os.environ.get("RUN_PLAN_COOL"):
+    import time
+    time.sleep(float(os.environ["RUN_PLAN_COOL"]))
 pplan = P.Plan(W.to_text(c), a.dtype, fuse=bool(a.fuse), profile=True)
 with P.StateVector(c.n, a.dtype) as sv:
     for _ in range(3):
