@@ -277,6 +277,7 @@ sv_status plan_schedule(sv_plan_s* p) {
     // ones (5) have one more free qubit; take that plan when it needs fewer passes (a 30 q
     // supremacy d20 circuit: 6 passes instead of 7, 21.8 -> 21.4 ms; the shorter runs cost
     // ~1 % of HBM bandwidth, tools/micro/seg_bw.cu)
+    int low = 0;
     if (!ctx.dbl && p->opts.use_jit() && p->opts.tile_qubits == 0 && !getenv("SV_LOW_QUBITS") && ctx.nl >= 14 &&
         p->sched.passes.size() > 1) {
         RunOpts o4 = p->opts;
@@ -291,9 +292,40 @@ sv_status plan_schedule(sv_plan_s* p) {
         }
         Schedule s4;
         if (!ops4.empty() && build_schedule(ops4, ctx, o4, s4, err, &p->lcirc) == SV_OK &&
-            s4.passes.size() < p->sched.passes.size())
+            s4.passes.size() < p->sched.passes.size()) {
             p->sched = std::move(s4);
+            low = 4;
+        }
         err.clear();
+    }
+    // Small states (every pass a handful of tiles, the one-kernel schedule of jit.cpp): the run
+    // is latency-bound on a few SMs, so fewer register bits per thread -- more threads per tile
+    // -- win whenever they do not cost a pass: the fewest passes, then the fewest register bits
+    // (12 q supremacy d10 complex128 11.3 -> 8.3 us, 16 q 16.7 -> 12.3 us; profiles/r02_small_rb.txt)
+    bool small = p->opts.use_jit() && p->opts.tile_qubits == 0 && !getenv("SV_RB") && !p->sched.passes.empty();
+    for (const PassPlan& pp : p->sched.passes)
+        small &= pp.kind == PassPlan::TILE && pp.sym && pp.ntiles > 0 && pp.ntiles <= 64;
+    if (small) {
+        const int rb0 = p->sched.passes[0].sym->rb;
+        for (int rb = rb0 - 1; rb >= 2; --rb) {
+            RunOpts o2 = p->opts;
+            o2.rb = rb;
+            o2.low_qubits = low;
+            std::vector<LOp> ops2;
+            bool ok = true;
+            for (size_t i = 0; i < p->lcirc.gates.size() && ok; ++i) {
+                bool needs_global = false;
+                ok = lower_gate(p->lcirc.gates[i], (int)i, ctx, o2, ops2, needs_global, err) == SV_OK;
+            }
+            Schedule s2;
+            if (ok && build_schedule(ops2, ctx, o2, s2, err, &p->lcirc) == SV_OK &&
+                s2.passes.size() <= p->sched.passes.size()) {
+                bool all_tile = true;
+                for (const PassPlan& pp : s2.passes) all_tile &= pp.kind == PassPlan::TILE && pp.sym != nullptr;
+                if (all_tile) p->sched = std::move(s2);
+            }
+            err.clear();
+        }
     }
     // a reversible circuit: one gather pass, unless its scattered reads cost more than the
     // fused tile passes (both estimated in HBM passes)

@@ -73,6 +73,7 @@ struct RunOpts {
     int exchange = 0;            // sharded: 0 = fused peer-memory exchange when available, 1 = NCCL
     bool no_rollout = false;     // internal: planning a rollout (no nested rollouts)
     int low_qubits = 0;          // internal: tile low positions (contiguous runs), 0 = default
+    int rb = 0;                  // internal: register bits per thread, 0 = default
     bool use_jit() const { return fuse && force_kernel == SV_KERNEL_AUTO; }
 };
 

@@ -766,7 +766,7 @@ sv_status build_schedule(std::vector<LOp>& ops, const Context& ctx_in, const Run
     Context ctx = ctx_in;
     const bool dbl = ctx.dbl;
     const int nl = ctx.nl;
-    const int rb = default_rb(dbl, nl);
+    const int rb = o.rb > 0 ? std::min(o.rb, nl) : default_rb(dbl, nl);
     static const int env_tile = [] {
         const char* e = getenv("SV_TILE_QUBITS");
         return e ? atoi(e) : 0;
