@@ -11,7 +11,9 @@ import paper_2106_13995_b200 as P  # noqa: E402
 
 torch.cuda.set_device(0)
 for dt in ("c128", "c64"):
-    for rows, cols in ((4, 3), (7, 2), (4, 4), (6, 3)):
+    import sys as _s
+    grids = ((4, 3), (7, 2), (4, 4), (6, 3)) if '--medium' not in _s.argv else ((6, 3), (5, 4), (11, 2), (6, 4))
+    for rows, cols in grids:
         c = W.supremacy(rows, cols, 10, seed=0)
         plan = P.Plan(W.to_text(c), dt)
         with P.StateVector(c.n, dt) as sv:
