@@ -10,10 +10,10 @@ import workloads as W  # noqa: E402
 import paper_2106_13995_b200 as P  # noqa: E402
 
 torch.cuda.set_device(0)
+# default: 12 / 14 / 16 / 18 q; --medium: 18 / 20 / 22 / 24 q
+GRIDS = ((6, 3), (5, 4), (11, 2), (6, 4)) if "--medium" in sys.argv else ((4, 3), (7, 2), (4, 4), (6, 3))
 for dt in ("c128", "c64"):
-    import sys as _s
-    grids = ((4, 3), (7, 2), (4, 4), (6, 3)) if '--medium' not in _s.argv else ((6, 3), (5, 4), (11, 2), (6, 4))
-    for rows, cols in grids:
+    for rows, cols in GRIDS:
         c = W.supremacy(rows, cols, 10, seed=0)
         plan = P.Plan(W.to_text(c), dt)
         with P.StateVector(c.n, dt) as sv:
