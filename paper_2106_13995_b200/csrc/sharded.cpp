@@ -351,6 +351,24 @@ sv_status exchange_one(sv_state_s* s, int j, std::string& err) {
     return SV_OK;
 }
 
+// SV_SHARD_ROLLOUT=1: the batches' relabelling schedules use the rollout search too (P plans
+// per process); SV_SHARD_LOW=L: L low tile positions for the batches (experiments)
+bool shard_rollout_enabled() {
+    static const bool b = [] {
+        const char* e = getenv("SV_SHARD_ROLLOUT");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return b;
+}
+
+int shard_low_qubits() {
+    static const int v = [] {
+        const char* e = getenv("SV_SHARD_LOW");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 bool shard_relabel_enabled() {
     static const bool b = [] {
         const char* e = getenv("SV_SHARD_RELABEL");
@@ -563,18 +581,41 @@ sv_status shard_plan(const Circuit& circ, const RunOpts& o, int n, int nl, int w
             bc.n = n;
             for (int gi : runnable) bc.gates.push_back(gates[gi]);
             RunOpts o2 = o;
-            o2.no_rollout = true;
-            std::vector<Schedule> all(world);
+            o2.no_rollout = !shard_rollout_enabled();
+            // every rank's plan for a number of low tile positions (complex64 also tries 4,
+            // 128-byte runs, as on one GPU: kept when it needs fewer passes; 30 q supremacy
+            // on 2 / 8 virtual shards 10 -> 9 passes, 30.1 -> 28.9 / 31.0 -> 29.6 ms)
+            auto plan_all = [&](int low, std::vector<Schedule>& all, std::vector<int>& endp) -> sv_status {
+                o2.low_qubits = low;
+                all.assign(world, Schedule());
+                endp.clear();
+                for (int r = 0; r < world; ++r) {
+                    std::vector<LOp> tmp;
+                    const sv_status st = build_schedule(tmp, ctx_for(r), o2, all[r], err, &bc);
+                    if (st != SV_OK) return st;
+                    const std::vector<int> e = all[r].end_phys.empty() ? phys : all[r].end_phys;
+                    if (r == 0) endp = e;
+                    else if (e != endp) return SV_ERR_STATE;  // maps differ: no relabelling
+                }
+                return SV_OK;
+            };
+            std::vector<Schedule> all;
             std::vector<int> endp;
-            bool same = true;
-            for (int r = 0; r < world && same; ++r) {
-                std::vector<LOp> tmp;
-                const sv_status st = build_schedule(tmp, ctx_for(r), o2, all[r], err, &bc);
-                if (st != SV_OK) return st;
-                const std::vector<int> e = all[r].end_phys.empty() ? phys : all[r].end_phys;
-                if (r == 0) endp = e;
-                else same = e == endp;
+            sv_status pst = plan_all(shard_low_qubits(), all, endp);
+            if (pst != SV_OK && pst != SV_ERR_STATE) return pst;
+            bool same = pst == SV_OK;
+            if (!ctx_for(0).dbl && !shard_low_qubits() && nl >= 14) {
+                std::vector<Schedule> all4;
+                std::vector<int> endp4;
+                const sv_status p4 = plan_all(4, all4, endp4);
+                if (p4 != SV_OK && p4 != SV_ERR_STATE) return p4;
+                if (p4 == SV_OK && (!same || all4[0].passes.size() < all[0].passes.size())) {
+                    all = std::move(all4);
+                    endp = std::move(endp4);
+                    same = true;
+                }
             }
+            err.clear();
             if (same) {
                 relabelled = true;
                 for (int i = 0; i < S; ++i) rsched[i] = std::move(all[ranks[i]]);
