@@ -273,26 +273,26 @@ sv_status plan_schedule(sv_plan_s* p) {
     }
     const sv_status st = build_schedule(ops, ctx, p->opts, p->sched, err, &p->lcirc);
     if (st != SV_OK) return fail(st, err);
+    // an alternative schedule of the same circuit under other tile options (internal RunOpts)
+    auto replan = [&](const RunOpts& o2, Schedule& s2) -> bool {
+        std::vector<LOp> ops2;
+        for (size_t i = 0; i < p->lcirc.gates.size(); ++i) {
+            bool needs_global = false;
+            if (lower_gate(p->lcirc.gates[i], (int)i, ctx, o2, ops2, needs_global, err) != SV_OK) return false;
+        }
+        return build_schedule(ops2, ctx, o2, s2, err, &p->lcirc) == SV_OK;
+    };
     // complex64: tiles whose low positions form 128-byte runs (4 qubits) instead of 256-byte
     // ones (5) have one more free qubit; take that plan when it needs fewer passes (a 30 q
-    // supremacy d20 circuit: 6 passes instead of 7, 21.8 -> 21.4 ms; the shorter runs cost
-    // ~1 % of HBM bandwidth, tools/micro/seg_bw.cu)
+    // supremacy d20 circuit: 6 passes instead of 7, 21.8 -> 21.4 ms; the shorter runs cost a
+    // light pass 1-6 % of its HBM rate, tools/micro/seg_bw.cu, profiles/r02_layout_ab.txt)
     int low = 0;
     if (!ctx.dbl && p->opts.use_jit() && p->opts.tile_qubits == 0 && !getenv("SV_LOW_QUBITS") && ctx.nl >= 14 &&
         p->sched.passes.size() > 1) {
         RunOpts o4 = p->opts;
         o4.low_qubits = 4;
-        std::vector<LOp> ops4;
-        for (size_t i = 0; i < p->lcirc.gates.size(); ++i) {
-            bool needs_global = false;
-            if (lower_gate(p->lcirc.gates[i], (int)i, ctx, o4, ops4, needs_global, err) != SV_OK) {
-                ops4.clear();
-                break;
-            }
-        }
         Schedule s4;
-        if (!ops4.empty() && build_schedule(ops4, ctx, o4, s4, err, &p->lcirc) == SV_OK &&
-            s4.passes.size() < p->sched.passes.size()) {
+        if (replan(o4, s4) && s4.passes.size() < p->sched.passes.size()) {
             p->sched = std::move(s4);
             low = 4;
         }
@@ -302,28 +302,19 @@ sv_status plan_schedule(sv_plan_s* p) {
     // is latency-bound on a few SMs, so fewer register bits per thread -- more threads per tile
     // -- win whenever they do not cost a pass: the fewest passes, then the fewest register bits
     // (12 q supremacy d10 complex128 11.3 -> 8.3 us, 16 q 16.7 -> 12.3 us; profiles/r02_small_rb.txt)
-    bool small = p->opts.use_jit() && p->opts.tile_qubits == 0 && !getenv("SV_RB") && !p->sched.passes.empty();
-    for (const PassPlan& pp : p->sched.passes)
-        small &= pp.kind == PassPlan::TILE && pp.sym && pp.ntiles > 0 && pp.ntiles <= 64;
-    if (small) {
-        const int rb0 = p->sched.passes[0].sym->rb;
-        for (int rb = rb0 - 1; rb >= 2; --rb) {
+    auto small_state = [](const Schedule& sc) {
+        bool ok = !sc.passes.empty();
+        for (const PassPlan& pp : sc.passes) ok &= pp.kind == PassPlan::TILE && pp.sym && pp.ntiles > 0 && pp.ntiles <= 64;
+        return ok;
+    };
+    if (p->opts.use_jit() && p->opts.tile_qubits == 0 && !getenv("SV_RB") && small_state(p->sched)) {
+        for (int rb = p->sched.passes[0].sym->rb - 1; rb >= 2; --rb) {
             RunOpts o2 = p->opts;
             o2.rb = rb;
             o2.low_qubits = low;
-            std::vector<LOp> ops2;
-            bool ok = true;
-            for (size_t i = 0; i < p->lcirc.gates.size() && ok; ++i) {
-                bool needs_global = false;
-                ok = lower_gate(p->lcirc.gates[i], (int)i, ctx, o2, ops2, needs_global, err) == SV_OK;
-            }
             Schedule s2;
-            if (ok && build_schedule(ops2, ctx, o2, s2, err, &p->lcirc) == SV_OK &&
-                s2.passes.size() <= p->sched.passes.size()) {
-                bool all_tile = true;
-                for (const PassPlan& pp : s2.passes) all_tile &= pp.kind == PassPlan::TILE && pp.sym != nullptr;
-                if (all_tile) p->sched = std::move(s2);
-            }
+            if (replan(o2, s2) && s2.passes.size() <= p->sched.passes.size() && small_state(s2))
+                p->sched = std::move(s2);
             err.clear();
         }
     }
