@@ -169,3 +169,20 @@ def test_basis_input_variant(P, dtype, k, monkeypatch):
     psi = np.zeros(1 << n, dtype=np.complex128)
     psi[k] = 1
     assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("seed", range(4))
+def test_supremacy_layouts_many_seeds(P, dtype, seed):
+    """Wider coverage of the shared-memory layout search (additive offsets, XOR bases, 16-byte
+    paired accesses, the barrier between a stage's reads and writes): supremacy circuits on
+    grids whose plans take 4-low-position tiles (14 q and up, complex64) and several seeds,
+    every pass executed on the host against the oracle."""
+    rows, cols = [(4, 4), (5, 3), (7, 2), (4, 4)][seed]
+    c = W.supremacy(rows, cols, 14, seed=10 + seed)
+    text = W.to_text(c)
+    psi = W.random_state(c.n, 20 + seed)
+    psi = W.round_to_c64(psi) if dtype == "c64" else psi
+    got, plan = _emulated(P, text, c.n, dtype, psi)
+    assert plan.info()["passes"] >= 2
+    assert_close(got, oracle.simulate(text, psi), dtype, W.gate_count(c))
