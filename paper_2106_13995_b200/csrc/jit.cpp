@@ -997,6 +997,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
         o << "struct alignas(16) C { R x, y; };\n";
         o << "__device__ __forceinline__ C mk(R x, R y){C c; c.x=x; c.y=y; return c;}\n";
         o << "__device__ __forceinline__ C CM(C a, C b){return mk(a.x*b.x-a.y*b.y, a.x*b.y+a.y*b.x);}\n";
+        o << "__device__ __forceinline__ unsigned long long W64(unsigned x){unsigned long long r;"
+             "asm(\"mov.b64 %0,{%1,%2};\":\"=l\"(r):\"r\"(x),\"r\"(0u));return r;}\n";
     } else {
         // packed complex64: lo = re, hi = im; paired FP32 ops (sm_100)
         o << "typedef unsigned long long C;\n"
@@ -1013,6 +1015,9 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
              "DI C NI(C a){return pk(hi(a),-lo(a));}\n"
              "DI C SX(C a,C s){return a^(s&0x8000000080000000ull);}\n"
              "DI C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}\n"
+             // a zero-extended 32-bit index the compiler cannot see is narrow (keeps the
+             // address arithmetic on LEA / LEA.HI.X instead of an IMAD.WIDE on the FMA pipe)
+             "DI unsigned long long W64(unsigned x){unsigned long long r;asm(\"mov.b64 %0,{%1,%2};\":\"=l\"(r):\"r\"(x),\"r\"(0u));return r;}\n"
              // stores as two 32-bit halves: with a b64 operand ptxas copies the pair into a
              // staging pair (2 MOVs per store, one issue cycle each in an FP-bound pass)
              "DI void SS(C* p,C v){asm volatile(\"st.shared.v2.f32 [%0],{%1,%2};\"::\"r\"((unsigned)__cvta_generic_to_shared(p)),"
@@ -1118,11 +1123,35 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
               << "__syncthreads();\nbase=tile_;\n";  // the previous tile's readers are done
         else o << "base=blockIdx.x;\n";
     }
-    if (!md.device_fn)
-        for (int b = 0; b < m; ++b) {
-            const int q = sym.tq[b];
-            o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
+    if (!md.device_fn) {
+        // tile base = the tile index with zeros inserted at the tile positions.  When every
+        // index fits 32 bits (log2(ntiles) + m <= 32), in 32-bit shifts and masks: the 64-bit
+        // form compiles to IMAD.WIDE on the FMA pipe, where a starting CTA's first instruction
+        // waits behind the other CTAs' paired FP ops (ncu: ~20 % of the stall samples of a
+        // balanced pass sat there, "math pipe throttle") and its loads go out late.
+        int lg = 0;
+        while (lg < 63 && (1ull << lg) < ntiles) ++lg;
+        static const bool narrow_ok = [] {
+            const char* e = getenv("SV_NARROW_BASE");
+            return e ? atoi(e) != 0 : true;
+        }();
+        const bool narrow = narrow_ok && !pf && !ploop && tpc == 1 && lg + m <= 32;
+        if (narrow) {
+            o << "{unsigned b32_=blockIdx.x;\n";
+            for (int b = 0; b < m; ++b) {
+                const int q = sym.tq[b];
+                o << "b32_=((b32_>>" << q << ")<<" << (q + 1) << ")|(b32_&" << ((1u << q) - 1) << "u);";
+            }
+            // (widened through inline asm: with a visibly zero high word ptxas narrows the
+            // address arithmetic to an IMAD.WIDE again; as a 64-bit value it stays LEA / LEA.HI.X)
+            o << "\nbase=W64(b32_);}\n";
+        } else {
+            for (int b = 0; b < m; ++b) {
+                const int q = sym.tq[b];
+                o << "base=((base>>" << q << ")<<" << (q + 1) << ")|(base&" << ((1ull << q) - 1) << "ull);\n";
+            }
         }
+    }
     // SV_L2PF = D > 0: L2 prefetch of the tile D tiles ahead (about the one a CTA of the next
     // wave will load): one cp.async.bulk.prefetch.L2 per 256-byte run of the tile (its low
     // qubits are physical 0..L-1), issued by the first 2^(m-L) threads

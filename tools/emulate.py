@@ -43,6 +43,7 @@ static inline C NI(C a){return pk(hi(a),-lo(a));}
 static inline C SX(C a,C s){return a^(s&0x8000000080000000ull);}
 static inline C CM(C a,C b){return pk(lo(a)*lo(b)-hi(a)*hi(b),lo(a)*hi(b)+hi(a)*lo(b));}
 static inline void SS(C* p,C v){*p=v;}
+static inline unsigned long long W64(unsigned x){return x;}
 static inline void SS2(C* p,C a,C b){p[0]=a;p[1]=b;}
 struct ulonglong2 { unsigned long long x, y; };
 static inline void SG(C* p,C v){*p=v;}
@@ -55,6 +56,7 @@ typedef double R;
 struct alignas(16) C { R x, y; };
 static inline C mk(R x, R y){C c; c.x=x; c.y=y; return c;}
 static inline C CM(C a, C b){return mk(a.x*b.x-a.y*b.y, a.x*b.y+a.y*b.x);}
+static inline unsigned long long W64(unsigned x){return x;}
 """
 
 _RUNNER = r"""
