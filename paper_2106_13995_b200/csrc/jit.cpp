@@ -1140,7 +1140,8 @@ std::string gen_pass_source(const TileSym& sym, uint64_t ntiles, int& threads, s
             o << "{unsigned b32_=blockIdx.x;\n";
             for (int b = 0; b < m; ++b) {
                 const int q = sym.tq[b];
-                o << "b32_=((b32_>>" << q << ")<<" << (q + 1) << ")|(b32_&" << ((1u << q) - 1) << "u);";
+                if (q >= 31) o << "b32_&=" << ((1u << q) - 1) << "u;";  // nothing above bit 31 (no shift by 32)
+                else o << "b32_=((b32_>>" << q << ")<<" << (q + 1) << ")|(b32_&" << ((1u << q) - 1) << "u);";
             }
             // (widened through inline asm: with a visibly zero high word ptxas narrows the
             // address arithmetic to an IMAD.WIDE again; as a 64-bit value it stays LEA / LEA.HI.X)

@@ -290,3 +290,19 @@ def test_plan_cache_concurrent_threads(P):
     for t in th:
         t.join()
     assert not errors, errors[:5]
+
+
+@pytest.mark.gpu
+def test_32q_mirror_with_top_tile_qubit(P):
+    """32 qubits on one GPU (complex64, 32 GiB): a tile containing qubit 31 takes the widest
+    32-bit tile-base computation (jit.cpp; no shift by 32); the circuit and its inverse return
+    |0...0> (mirror, S:212)."""
+    c = W.supremacy(7, 5, 20, 0, n=32)
+    plan = P.Plan(W.to_text(c), "c64")
+    assert any("b32_&=" in plan.source(i) for i in range(plan.info()["passes"]))
+    m = W.concat(c, W.inverse(c))
+    with P.StateVector(32, "c64") as sv:
+        sv.apply_circuit(W.to_text(m))
+        a = sv.amplitudes(0, 4)
+        nrm = sv.norm()
+    assert abs(a[0] - 1) < 1e-3 and np.max(np.abs(a[1:])) < 1e-4 and abs(nrm - 1) < 1e-3
