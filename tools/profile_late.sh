@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-3 captures (run under gpurun): --set full of c64 passes 0 (basis variant), 2, 3 and c128
 # pass 3 of the second run of the plan; raw + details CSV exported for tools/ncu_summary.py.
-R=${1:-r03}
+R=${1:-late}
 OUT=gpurun_out/profile_$R
 mkdir -p $OUT
 for spec in c64:7:p0 c64:9:p2 c64:10:p3 c128:10:p3; do
