@@ -691,8 +691,11 @@ double heavy_pass_cost(bool dbl) {
         const char* e = getenv("SV_HEAVY_COST128");
         // c128: 52.7 ms at 200, 52.6 at 160, 54.6 at 130, 57.4 at 100 (8-pass plan); with the
         // 7-pass rollout plan 130 and 160 are within run-to-run noise (three repeats each:
-        // 45.8-46.9 vs 45.8-47.1 ms, profiles/r01_heavy_sweep.txt)
-        return e ? atof(e) : 160.0;
+        // 45.8-46.9 vs 45.8-47.1 ms, profiles/r01_heavy_sweep.txt).  End of round 2, under ncu
+        // with locked base clocks (power capping makes the free-running c128 numbers swing by
+        // +-4 %): the 176-unit pass 16.72 ms with one register bit fewer, 16.10 ms without; 200
+        // (tools/ncu_ab.sh, profiles/r02_ncu_ab_c128.txt)
+        return e ? atof(e) : 200.0;
     }();
     return dbl ? b2 : b;
 }
