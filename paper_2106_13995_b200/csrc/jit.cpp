@@ -889,7 +889,8 @@ int tiles_per_cta() {
 
 // CTAs per SM the register allocation must allow (SV_MIN_WARPS: resident warps per SM).
 // Measured (profiles/r01_min_warps.txt, 30 q supremacy): c64 24.85 ms at 16 warps, 24.2 at
-// 20, 27.6 at 24; c128 no better than noise at 20, 62 ms at 24 -- 20 (c64) / 16 (c128).
+// 20, 27.6 at 24; c128 no better than noise at 20, 62 ms at 24 -- 20 (c64) / 16 (c128); 20 for
+// both since the end of round 2 (below).
 int min_blocks(int threads, bool dbl, bool heavy = false) {
     static const int w = [] {
         const char* e = getenv("SV_MIN_WARPS");
@@ -900,7 +901,10 @@ int min_blocks(int threads, bool dbl, bool heavy = false) {
         const char* e = getenv("SV_MIN_WARPS_HEAVY");
         return e ? atoi(e) : 0;
     }();
-    const int warps = (heavy && wh > 0) ? wh : w > 0 ? w : dbl ? 16 : 20;
+    // complex128 16 -> 20 at the end of round 2: with the smaller generated code its passes
+    // fit 5 CTAs (<= 102 registers) without spilling; serialized ncu timing (tools/ncu_ab.sh,
+    // CLOCK=none) 30 q c128 pass 1 6.80 -> 6.39 ms, pass 3 9.48 -> 9.27 ms (24: 45 ms, spills)
+    const int warps = (heavy && wh > 0) ? wh : w > 0 ? w : 20;
     return std::max(1, std::min(32, warps * 32 / threads));
 }
 
